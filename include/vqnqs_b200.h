@@ -1,0 +1,146 @@
+/* vqnqs_b200 — C ABI of the B200-native local-energy engine.
+ *
+ * This is the drop-in boundary for the reference's local-energy path. The
+ * reference exposes it as C++ (proj/include/vqnqs/trainer.hpp:76-79,
+ * proj/include/vqnqs/dedup.hpp:77-93); a C++ caller keeps those signatures by
+ * going through the header-only adapter include/vqnqs_b200.hpp, which calls
+ * the functions below. Plain pointers and sizes only — no torch, no STL.
+ *
+ * Status codes mirror the reference's exception taxonomy
+ * (proj/include/vqnqs/common.hpp:14-28); the adapter re-throws them as the
+ * matching vqnqs::*Error. The message of the last failure on the calling
+ * thread is vqnqs_last_error().
+ *
+ * A handle is bound to one CUDA device and is not thread-safe: serialise
+ * calls on it (the reference's worker pool becomes one handle per GPU).
+ */
+#ifndef VQNQS_B200_H
+#define VQNQS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  VQNQS_OK = 0,
+  VQNQS_CONFIG_ERROR = 1,     /* vqnqs::ConfigError */
+  VQNQS_SHAPE_ERROR = 2,      /* vqnqs::ShapeError (check()) */
+  VQNQS_CAPABILITY_ERROR = 3, /* vqnqs::CapabilityError */
+  VQNQS_NUMERIC_ERROR = 4,    /* vqnqs::NumericError (non-finite E_loc) */
+  VQNQS_USAGE_ERROR = 5,      /* vqnqs::UsageError */
+  VQNQS_RUNTIME_ERROR = 6     /* CUDA / allocation failure */
+};
+
+enum { VQNQS_PREC_FP32 = 0, VQNQS_PREC_BF16 = 1 };
+
+/* Field-for-field subset of vqnqs::ModelConfig
+ * (proj/include/vqnqs/model.hpp:13-27); local_dim is fixed at 2. */
+typedef struct {
+  int32_t n_sites, group_size, d_hidden, n_heads, n_blocks;
+  int32_t trailing_half_block, vq_enabled, vq_heads, vq_codebook, phase_enabled;
+  double vq_init_scale;
+} vqnqs_model_desc;
+
+typedef struct vqnqs_handle vqnqs_handle;
+
+/* Ledger slots, in the order of flops::Ledger's fields
+ * (proj/include/vqnqs/flops.hpp:12-44). */
+enum {
+  VQNQS_LEDGER_PER_LOCATION_DENSE = 0,
+  VQNQS_LEDGER_PER_LOCATION_UNIQUE = 1,
+  VQNQS_LEDGER_ATTENTION = 2,
+  VQNQS_LEDGER_VQ_DISTANCE = 3,
+  VQNQS_LEDGER_OTHER = 4,
+  VQNQS_LEDGER_PER_LOCATION_DENSE_QUANTIZED = 5,
+  VQNQS_LEDGER_PER_LOCATION_UNIQUE_QUANTIZED = 6,
+  VQNQS_LEDGER_SLOTS = 7
+};
+
+const char* vqnqs_last_error(void);
+
+/* ---- host-side model/lattice helpers (no GPU needed) ---- */
+
+/* Number of parameter tensors and the numel of each, in the reference's
+ * parameters() order (proj/src/model.cpp:210-229). numels may be NULL. */
+int vqnqs_param_layout(const vqnqs_model_desc* d, int* n_params, int64_t* numels);
+
+/* VqTransformer::init(cfg, Rng(seed)) (proj/src/model.cpp:150-184): fills the
+ * caller's float64 buffers (parameters() order, sizes from
+ * vqnqs_param_layout). snap_bf16 rounds every value to bf16. */
+int vqnqs_init_params(const vqnqs_model_desc* d, uint64_t seed, int snap_bf16,
+                      double* const* params);
+
+/* Lattice bonds (proj/src/hamiltonian.cpp:5-35); periodic=1 adds the wrap
+ * bonds of SURVEY §8d. ly=0 for chains. Returns the bond count (writes at
+ * most cap pairs), or -status. */
+int vqnqs_build_lattice(int lx, int ly, int periodic, int32_t* bonds, int cap);
+
+/* Zero-Sz configurations: sample i <- Rng(seed).split(start + i), N/2 up
+ * spins shuffled by Fisher-Yates. out is [count x n]. */
+int vqnqs_zero_sz_samples(int n, int64_t start, int64_t count, uint64_t seed,
+                          uint8_t* out);
+
+/* ---- engine ---- */
+
+/* Uploads weights (float64, parameters() order) to `device`, converting to
+ * the engine precision. Validates like ModelConfig::validate
+ * (proj/src/model.cpp:10-27). Replaces constructing a VqTransformer for the
+ * GPU: the handle plays the role of `const VqTransformer&`. */
+int vqnqs_gpu_create(const vqnqs_model_desc* d, const double* const* params,
+                     int n_params, int precision, int device, vqnqs_handle** out);
+
+/* Heisenberg Hamiltonian on an explicit bond list [nb][2] (the fields
+ * connected_set reads, proj/src/hamiltonian.cpp:41-74). TFIM is refused
+ * with VQNQS_CAPABILITY_ERROR. Plays the role of `const HamiltonianModel&`. */
+int vqnqs_gpu_set_hamiltonian(vqnqs_handle* h, const int32_t* bonds, int nb,
+                              int n_sites, int marshall);
+
+/* Replaces local_energies(model, h, batch, ledger)
+ * (proj/include/vqnqs/trainer.hpp:76-79, proj/src/trainer.cpp:150-180).
+ * configs: host [B x n_sites] bytes (0 = down, 1 = up). Outputs host arrays
+ * of B doubles; e_im/logpsi/ledger7 may be NULL. logpsi = 0.5 * log P(s)
+ * (proj/src/model.cpp:481-483). ledger7 is ADDED to (like
+ * `*ledger += part`, trainer.cpp:177-178). Synchronous. A non-finite E_loc
+ * returns VQNQS_NUMERIC_ERROR naming the configuration, like the reference. */
+int vqnqs_gpu_local_energies(vqnqs_handle* h, const uint8_t* configs, int64_t B,
+                             double* e_re, double* e_im, double* logpsi,
+                             int64_t* ledger7);
+
+/* Same, on device buffers (configs, e_re, logpsi on the handle's device),
+ * ordered on `stream` (a cudaStream_t, NULL = the handle's own stream).
+ * Returns after enqueueing the last kernel for this batch; the ledger (host)
+ * is filled after the engine's per-chunk size readbacks. */
+int vqnqs_gpu_local_energies_device(vqnqs_handle* h, const uint8_t* d_configs,
+                                    int64_t B, double* d_e_re, double* d_logpsi,
+                                    int64_t* ledger7, void* stream);
+
+/* Replaces dedup_log_prob(model, configs, base) (proj/include/vqnqs/dedup.hpp:77-79)
+ * for the connected set of `base`: per-row log-probs lp[K] in connected_set
+ * order (diagonal first, then bond order). Returns K (>0) or -status. */
+int vqnqs_gpu_connected_log_probs(vqnqs_handle* h, const uint8_t* base,
+                                  double* lp, int cap);
+
+/* Parity taps for a batch (same layout as the oracle's taps):
+ *   K[B], U[B*(L+1)], codes[sum_s K_s*T*L] (layer-major per sample:
+ *   sample s occupies L*K_s*T entries, [layer][row][pos]),
+ *   lp_rows[sum_s K_s] per-row log-probs in connected_set order.
+ * Returns 0 or status. Any output pointer may be NULL. */
+int vqnqs_gpu_taps(vqnqs_handle* h, const uint8_t* configs, int64_t B,
+                   int32_t* K, int64_t* U, int32_t* codes, int64_t codes_cap,
+                   double* lp_rows, int64_t lp_cap);
+
+/* Kernel launches issued by the last local-energies call (own kernels only). */
+int64_t vqnqs_gpu_last_launch_count(vqnqs_handle* h);
+
+/* Per-call timings of the last call's dominant kernel family (ms, CUDA events
+ * on the engine stream) and its algorithmic bytes/flops; see DESIGN.md. */
+int vqnqs_gpu_last_profile(vqnqs_handle* h, double* out, int cap);
+
+int vqnqs_gpu_destroy(vqnqs_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VQNQS_B200_H */

@@ -1,0 +1,170 @@
+// C ABI (include/vqnqs_b200.h): exception -> status translation around the
+// engine. Mirrors how the reference surfaces failures (typed exceptions,
+// proj/include/vqnqs/common.hpp:14-28) as integer status codes plus a
+// thread-local message.
+#include <cstring>
+#include <exception>
+#include <vector>
+#include <string>
+
+#include "engine.h"
+
+struct vqnqs_handle {
+  vqb::Engine* eng;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return VQNQS_OK;
+  } catch (const vqb::Error& e) {
+    g_err = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return VQNQS_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VQNQS_RUNTIME_ERROR;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* vqnqs_last_error(void) { return g_err.c_str(); }
+
+int vqnqs_param_layout(const vqnqs_model_desc* d, int* n_params, int64_t* numels) {
+  return guarded([&] {
+    if (!d) throw vqb::UsageError("null model descriptor");
+    auto spec = vqb::param_layout(*d);
+    if (n_params) *n_params = int(spec.size());
+    if (numels)
+      for (size_t i = 0; i < spec.size(); ++i) numels[i] = spec[i].rows * spec[i].cols;
+  });
+}
+
+int vqnqs_init_params(const vqnqs_model_desc* d, uint64_t seed, int snap_bf16,
+                      double* const* params) {
+  return guarded([&] {
+    if (!d || !params) throw vqb::UsageError("null argument");
+    vqb::init_params(*d, seed, snap_bf16 != 0, params);
+  });
+}
+
+int vqnqs_build_lattice(int lx, int ly, int periodic, int32_t* bonds, int cap) {
+  int nb = 0;
+  int st = guarded([&] {
+    auto b = vqb::build_lattice(lx, ly, periodic != 0);
+    nb = int(b.size() / 2);
+    if (bonds) std::memcpy(bonds, b.data(), sizeof(int32_t) * 2 * size_t(std::min(nb, cap)));
+  });
+  return st == 0 ? nb : -st;
+}
+
+int vqnqs_zero_sz_samples(int n, int64_t start, int64_t count, uint64_t seed, uint8_t* out) {
+  return guarded([&] {
+    if (n < 1 || count < 0 || !out) throw vqb::UsageError("bad sampler arguments");
+    vqb::zero_sz_samples(n, start, count, seed, out);
+  });
+}
+
+int vqnqs_gpu_create(const vqnqs_model_desc* d, const double* const* params, int n_params,
+                     int precision, int device, vqnqs_handle** out) {
+  return guarded([&] {
+    if (!d || !params || !out) throw vqb::UsageError("null argument");
+    *out = nullptr;
+    auto* h = new vqnqs_handle{nullptr};
+    try {
+      h->eng = new vqb::Engine(*d, params, n_params, precision, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int vqnqs_gpu_set_hamiltonian(vqnqs_handle* h, const int32_t* bonds, int nb, int n_sites,
+                              int marshall) {
+  return guarded([&] {
+    if (!h) throw vqb::UsageError("null handle");
+    h->eng->set_hamiltonian(bonds, nb, n_sites, marshall != 0);
+  });
+}
+
+int vqnqs_gpu_local_energies(vqnqs_handle* h, const uint8_t* configs, int64_t B, double* e_re,
+                             double* e_im, double* logpsi, int64_t* ledger7) {
+  return guarded([&] {
+    if (!h || (!configs && B > 0) || (!e_re && B > 0)) throw vqb::UsageError("null argument");
+    if (B <= 0) return;
+    const int n = h->eng->desc().n_sites;
+    for (int64_t i = 0; i < B * n; ++i)
+      if (configs[i] > 1) throw vqb::ConfigError("configuration entries must be 0 or 1");
+    h->eng->run_host(configs, B, e_re, e_im, logpsi, ledger7, nullptr);
+  });
+}
+
+int vqnqs_gpu_local_energies_device(vqnqs_handle* h, const uint8_t* d_configs, int64_t B,
+                                    double* d_e_re, double* d_logpsi, int64_t* ledger7,
+                                    void* stream) {
+  return guarded([&] {
+    if (!h) throw vqb::UsageError("null handle");
+    if (B <= 0) return;
+    h->eng->run_device(d_configs, B, d_e_re, d_logpsi, ledger7, stream, nullptr);
+  });
+}
+
+int vqnqs_gpu_connected_log_probs(vqnqs_handle* h, const uint8_t* base, double* lp, int cap) {
+  int K = 0;
+  int st = guarded([&] {
+    if (!h || !base) throw vqb::UsageError("null argument");
+    int32_t Kv = 0;
+    std::vector<double> rows(static_cast<size_t>(std::max(cap, 1)) + 4096);
+    vqb::Engine::Taps t;
+    t.K = &Kv;
+    t.lp_rows = rows.data();
+    t.lp_cap = int64_t(rows.size());
+    double e, lpsi;
+    h->eng->run_host(base, 1, &e, nullptr, &lpsi, nullptr, &t);
+    K = Kv;
+    if (lp) std::memcpy(lp, rows.data(), sizeof(double) * size_t(std::min(K, cap)));
+  });
+  return st == 0 ? K : -st;
+}
+
+int vqnqs_gpu_taps(vqnqs_handle* h, const uint8_t* configs, int64_t B, int32_t* K, int64_t* U,
+                   int32_t* codes, int64_t codes_cap, double* lp_rows, int64_t lp_cap) {
+  return guarded([&] {
+    if (!h || !configs) throw vqb::UsageError("null argument");
+    vqb::Engine::Taps t;
+    t.K = K;
+    t.U = U;
+    t.codes = codes;
+    t.codes_cap = codes_cap;
+    t.lp_rows = lp_rows;
+    t.lp_cap = lp_cap;
+    std::vector<double> e(static_cast<size_t>(B)), lpsi(static_cast<size_t>(B));
+    h->eng->run_host(configs, B, e.data(), nullptr, lpsi.data(), nullptr, &t);
+  });
+}
+
+int64_t vqnqs_gpu_last_launch_count(vqnqs_handle* h) { return h ? h->eng->last_launches() : -1; }
+
+int vqnqs_gpu_last_profile(vqnqs_handle* h, double* out, int cap) {
+  return h ? h->eng->last_profile(out, cap) : -1;
+}
+
+int vqnqs_gpu_destroy(vqnqs_handle* h) {
+  return guarded([&] {
+    if (!h) return;
+    delete h->eng;
+    delete h;
+  });
+}
+
+}  // extern "C"

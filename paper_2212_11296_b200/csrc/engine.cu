@@ -1,0 +1,657 @@
+// Host orchestration of the local-energy pipeline on one B200.
+//
+// One call = one batch of B sample configurations, processed in micro-batches
+// ("chunks") of at most S samples. Per chunk:
+//   (a) k_connected / k_scan / k_enumerate   connected sets, active locations
+//   (d) k_dedup<0> + k_embed                 unique input rows
+//   per block b:
+//   (b) LN1 -> QKV GEMM on U_b unique rows   k_layernorm, gemm
+//   (b) gathered causal attention            attention over active locations
+//   (c) nearest codeword                     vq
+//   (d) requantize dedup + gather build      k_dedup<1>, k_build_gather
+//   (b) continuation GEMM chain on U_{b+1}   gemm(Wo)+resid, LN2, gemm(W1)+gelu, gemm(W2)+resid
+//   (e) LN_f + head + log_softmax, E_loc     k_layernorm, k_head, k_eloc
+// The only host synchronisation per chunk is one 16-byte readback of the
+// chunk's active-location/table totals (to size the arena) and the final
+// U-count readback for the ledger.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <vector>
+
+#include "common.cuh"
+#include "engine.h"
+#include "pipeline_kernels.cuh"
+#include "simt_kernels.cuh"
+#include "tc_kernels.cuh"
+
+namespace vqb {
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      throw RuntimeError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                         __FILE__ + ":" + std::to_string(__LINE__));                   \
+  } while (0)
+
+namespace {
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t want) {
+    if (want <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    size_t alloc = std::max<size_t>(want + want / 4, 64);
+    cudaError_t e = cudaMalloc(&p, alloc * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw RuntimeError(std::string("device allocation failed: ") + cudaGetErrorString(e));
+    }
+    n = alloc;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct DevBlock {
+  float *ln1_g, *ln1_b, *bqkv, *bo, *ln2_g, *ln2_b, *b1, *b2, *cb32;
+  void *wqkv, *wo, *w1, *w2, *cbA;       // [in x out] row-major, operand type
+  void *wqkvT, *woT, *w1T, *w2T;         // [out x in] (K-major) copies for tcgen05
+};
+
+}  // namespace
+
+void ledger_add(const vqnqs_model_desc& c, int64_t K, const int64_t* U, int64_t* led) {
+  // proj/src/flops.cpp:29-72 with opcost (tensor.hpp:81-102); the dense
+  // shadow scales each per-location segment's exact per-row cost to K*T.
+  const int64_t T = (c.n_sites + c.group_size - 1) / c.group_size, KT = K * T;
+  const int64_t d = c.d_hidden, V = int64_t(1) << c.group_size;
+  auto per_loc = [&](int64_t u, int64_t cost, bool q) {
+    led[1] += cost;
+    if (q) led[6] += cost;
+    const int64_t dense = (u > 0 && cost % u == 0) ? cost / u * KT : cost;
+    led[0] += dense;
+    if (q) led[5] += dense;
+  };
+  per_loc(U[0], U[0] * d, false);
+  const int nblk = c.n_blocks + (c.trailing_half_block ? 1 : 0);
+  bool seen_vq = false;
+  for (int b = 0; b < nblk; ++b) {
+    const bool half = b == c.n_blocks;
+    const bool has_vq = !half && c.vq_enabled;
+    const bool pre_q = c.vq_enabled && seen_vq, cont_q = c.vq_enabled && (seen_vq || has_vq);
+    const int64_t u = U[b], u2 = U[b + 1];
+    per_loc(u, u * (7 * d + 5), pre_q);
+    for (int i = 0; i < 3; ++i) per_loc(u, 2 * u * d * d + u * d, pre_q);
+    const int64_t nh = c.n_heads, dh = d / nh;
+    led[2] += K * nh * (4 * T * T * dh + 6 * T * T);
+    if (has_vq) {
+      const int64_t H = c.vq_heads, vdh = d / H, Q = c.vq_codebook;
+      led[3] += KT * H * (Q * (3 * vdh + 2) + Q);
+    }
+    int64_t cost = 2 * u2 * d * d + u2 * d + u2 * d;
+    if (!half)
+      cost += u2 * (7 * d + 5) + 2 * u2 * d * 4 * d + u2 * 4 * d + 10 * u2 * 4 * d +
+              2 * u2 * 4 * d * d + u2 * d + u2 * d;
+    per_loc(u2, cost, cont_q);
+    seen_vq = seen_vq || has_vq;
+  }
+  const int64_t uL = U[nblk];
+  const bool head_q = c.vq_enabled && seen_vq;
+  per_loc(uL, uL * (7 * d + 5), head_q);
+  per_loc(uL, 2 * uL * d * V + uL * V, head_q);
+  per_loc(uL, uL * (5 * V + 1), head_q);
+  led[4] += KT;
+}
+
+class EngineImpl {
+ public:
+  vqnqs_model_desc c{};
+  int prec = VQNQS_PREC_FP32;
+  int dev = 0;
+  int sms = 148;
+  cudaStream_t own = nullptr;
+  int d, nh, dh, Q, L, V, T, g, N, lastV;
+  bool use_tc = false;  // tcgen05 paths (bf16 precision)
+  std::vector<void*> allocs;
+  float *tok_embed, *pos_embed, *lnf_g, *lnf_b, *head_b;
+  void* head_w;
+  std::vector<DevBlock> blk;
+  // hamiltonian
+  int nb = 0;
+  bool marshall = true;
+  int32_t* d_bonds = nullptr;
+  std::vector<int32_t> h_bonds;
+  // launch accounting / profile
+  int64_t launches = 0;
+  double prof[8] = {0};
+  // arena
+  int S_max = 256;
+  DBuf<int32_t> K_, Mact_, row_bond_, row_t1_, tok0_, lrow_, Ucnt_, I_a, I_b, code_, slot_,
+      rep_of_, trep_, tuid_, g_code_;
+  DBuf<int16_t> lpos_, upos_;
+  DBuf<int64_t> row_aoff_, act_off_, tab_off_, Uoff_, tot_, g_res_, attw_;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  DBuf<double> diag_, lpV_, lp_rows_;
+  DBuf<unsigned long long> tkey_;
+  DBuf<float> x_a, x_b, y_, att_;
+  DBuf<char> h_, qkv_, f1_;
+  DBuf<uint8_t> cfg_stage_;
+  DBuf<double> out_stage_;
+  DBuf<int32_t> taps_codes_;
+  size_t tab_cap_n = 0;
+  uint8_t* h_pinned_cfg = nullptr;
+  size_t h_pinned_cfg_n = 0;
+  double* h_pinned_out = nullptr;
+  size_t h_pinned_out_n = 0;
+
+  size_t esz() const { return prec == VQNQS_PREC_BF16 ? 2 : 4; }
+
+  template <typename T>
+  T* upload(const std::vector<T>& v) {
+    T* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(v.size(), 1) * sizeof(T)));
+    CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    allocs.push_back(p);
+    return p;
+  }
+  void* upload_op(const std::vector<double>& v) {
+    if (prec == VQNQS_PREC_BF16) {
+      std::vector<uint16_t> b(v.size());
+      for (size_t i = 0; i < v.size(); ++i) {
+        float f = static_cast<float>(v[i]);
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        if ((u & 0x7f800000u) != 0x7f800000u) u += 0x7fffu + ((u >> 16) & 1u);
+        b[i] = static_cast<uint16_t>(u >> 16);
+      }
+      return upload(b);
+    }
+    std::vector<float> f(v.begin(), v.end());
+    return upload(f);
+  }
+  float* upload_f(const double* p, int64_t n) {
+    std::vector<float> f(p, p + n);
+    return upload(f);
+  }
+
+  EngineImpl(const vqnqs_model_desc& desc, const double* const* params, int n_params, int precision,
+             int device)
+      : c(desc), prec(precision), dev(device) {
+    auto spec = param_layout(c);
+    if (n_params != int(spec.size()))
+      throw ShapeError("parameter count " + std::to_string(n_params) + " != " +
+                       std::to_string(spec.size()));
+    if (!c.vq_enabled || c.trailing_half_block)
+      throw CapabilityError("GPU path: every block must carry a VQ (no half block, vq on)");
+    if (c.vq_heads != 1) throw CapabilityError("GPU path: vq_heads must be 1");
+    if (c.group_size > 4) throw CapabilityError("GPU path: group_size <= 4");
+    if (c.d_hidden % 16 != 0) throw CapabilityError("GPU path: d_hidden % 16 == 0");
+    if (precision != VQNQS_PREC_FP32 && precision != VQNQS_PREC_BF16)
+      throw ConfigError("precision must be fp32 or bf16");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw RuntimeError("no such CUDA device");
+    CK(cudaSetDevice(dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+    d = c.d_hidden;
+    nh = c.n_heads;
+    dh = d / nh;
+    Q = c.vq_codebook;
+    L = c.n_blocks;
+    g = c.group_size;
+    V = 1 << g;
+    N = c.n_sites;
+    T = (N + g - 1) / g;
+    lastV = (N % g == 0) ? V : 1 << (N % g);
+    if (T > 1024 || dh > 256) throw CapabilityError("GPU path: T <= 1024, head dim <= 256");
+    use_tc = tc_supported(prec, d, dh, T, Q);
+    // weights, parameters() order (proj/src/model.cpp:188-229)
+    int i = 0;
+    auto nxt = [&]() -> const double* { return params[i++]; };
+    auto numel = [&](int j) { return spec[j].rows * spec[j].cols; };
+    tok_embed = upload_f(nxt(), numel(0));
+    pos_embed = upload_f(nxt(), numel(1));
+    for (int b = 0; b < L; ++b) {
+      DevBlock B{};
+      const double* ln1g = nxt();
+      const double* ln1b = nxt();
+      const double *wq = nxt(), *bq = nxt(), *wk = nxt(), *bk = nxt(), *wv = nxt(), *bv = nxt(),
+                   *wo = nxt(), *bo = nxt(), *cb = nxt();
+      const double *ln2g = nxt(), *ln2b = nxt(), *w1 = nxt(), *b1 = nxt(), *w2 = nxt(),
+                   *b2 = nxt();
+      B.ln1_g = upload_f(ln1g, d);
+      B.ln1_b = upload_f(ln1b, d);
+      std::vector<double> wqkv((size_t)d * 3 * d), bqkv(3 * d);
+      for (int r = 0; r < d; ++r)
+        for (int cc = 0; cc < d; ++cc) {
+          wqkv[(size_t)r * 3 * d + cc] = wq[(size_t)r * d + cc];
+          wqkv[(size_t)r * 3 * d + d + cc] = wk[(size_t)r * d + cc];
+          wqkv[(size_t)r * 3 * d + 2 * d + cc] = wv[(size_t)r * d + cc];
+        }
+      for (int cc = 0; cc < d; ++cc) {
+        bqkv[cc] = bq[cc];
+        bqkv[d + cc] = bk[cc];
+        bqkv[2 * d + cc] = bv[cc];
+      }
+      B.wqkv = upload_op(wqkv);
+      B.bqkv = upload_f(bqkv.data(), 3 * d);
+      B.wo = upload_op(std::vector<double>(wo, wo + (size_t)d * d));
+      B.bo = upload_f(bo, d);
+      B.cb32 = upload_f(cb, (int64_t)Q * d);
+      B.cbA = upload_op(std::vector<double>(cb, cb + (size_t)Q * d));
+      B.ln2_g = upload_f(ln2g, d);
+      B.ln2_b = upload_f(ln2b, d);
+      B.w1 = upload_op(std::vector<double>(w1, w1 + (size_t)d * 4 * d));
+      B.b1 = upload_f(b1, 4 * d);
+      B.w2 = upload_op(std::vector<double>(w2, w2 + (size_t)4 * d * d));
+      B.b2 = upload_f(b2, d);
+      if (use_tc) {
+        auto tr = [](const double* w, int rows, int cols) {
+          std::vector<double> t((size_t)rows * cols);
+          for (int r = 0; r < rows; ++r)
+            for (int cc = 0; cc < cols; ++cc) t[(size_t)cc * rows + r] = w[(size_t)r * cols + cc];
+          return t;
+        };
+        B.wqkvT = upload_op(tr(wqkv.data(), d, 3 * d));
+        B.woT = upload_op(tr(wo, d, d));
+        B.w1T = upload_op(tr(w1, d, 4 * d));
+        B.w2T = upload_op(tr(w2, 4 * d, d));
+      }
+      blk.push_back(B);
+    }
+    lnf_g = upload_f(nxt(), d);
+    lnf_b = upload_f(nxt(), d);
+    head_w = upload_op(std::vector<double>(params[i], params[i] + (size_t)d * V));
+    ++i;
+    head_b = upload_f(nxt(), V);
+  }
+
+  ~EngineImpl() {
+    cudaSetDevice(dev);
+    for (void* p : allocs) cudaFree(p);
+    DBufRelease();
+    if (d_bonds) cudaFree(d_bonds);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (own) cudaStreamDestroy(own);
+    if (h_pinned_cfg) cudaFreeHost(h_pinned_cfg);
+    if (h_pinned_out) cudaFreeHost(h_pinned_out);
+  }
+  void DBufRelease() {
+    K_.release(); Mact_.release(); row_bond_.release(); row_t1_.release(); tok0_.release();
+    lrow_.release(); Ucnt_.release(); I_a.release(); I_b.release(); code_.release();
+    slot_.release(); rep_of_.release(); trep_.release(); tuid_.release(); g_code_.release();
+    lpos_.release(); upos_.release(); row_aoff_.release(); act_off_.release(); tab_off_.release();
+    Uoff_.release(); tot_.release(); g_res_.release(); attw_.release(); diag_.release(); lpV_.release();
+    lp_rows_.release(); tkey_.release(); x_a.release(); x_b.release(); y_.release();
+    att_.release(); h_.release(); qkv_.release(); f1_.release(); cfg_stage_.release();
+    out_stage_.release(); taps_codes_.release();
+  }
+
+  void set_hamiltonian(const int32_t* bonds, int nbonds, int n_sites, bool m) {
+    if (n_sites != N) throw ShapeError("configuration size != site count");
+    if (nbonds < 0) throw ConfigError("negative bond count");
+    for (int b = 0; b < nbonds; ++b) {
+      const int i = bonds[2 * b], j = bonds[2 * b + 1];
+      if (i < 0 || j < 0 || i >= N || j >= N || i == j)
+        throw ConfigError("bond " + std::to_string(b) + " out of range");
+    }
+    CK(cudaSetDevice(dev));
+    if (d_bonds) cudaFree(d_bonds);
+    d_bonds = nullptr;
+    h_bonds.assign(bonds, bonds + 2 * nbonds);
+    CK(cudaMalloc(&d_bonds, std::max(1, 2 * nbonds) * sizeof(int32_t)));
+    CK(cudaMemcpy(d_bonds, bonds, 2 * nbonds * sizeof(int32_t), cudaMemcpyHostToDevice));
+    nb = nbonds;
+    marshall = m;
+    // micro-batch size: keep the per-location working set near a fixed budget
+    const double locs = double(T) + double(nb) * 0.5 * double(T);  // ~ active per sample
+    const double bytes_per_loc = double(d) * (use_tc ? 24.0 : 40.0) + 64.0;
+    const double budget = 24e9;
+    S_max = int(std::clamp(budget / (locs * bytes_per_loc), 16.0, 4096.0));
+  }
+
+  template <typename TA>
+  void gemm(const int64_t* Mp, int64_t Mcap, int Nn, int Kk, const void* A, int lda,
+            const int32_t* gA, const void* B, const void* BT, const float* bias, void* out, int ldo,
+            int epi, const float* resid, int ldr, const int64_t* gR, cudaStream_t st) {
+    if (use_tc && BT) {
+      tc_gemm(Mp, Mcap, Nn, Kk, A, lda, gA, BT, bias, out, ldo, epi, resid, ldr, gR, st, sms);
+      ++launches;
+      return;
+    }
+    const int64_t tiles = ((Mcap + 63) / 64) * ((Nn + 63) / 64);
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sms) * 8)));
+    const TA* a = static_cast<const TA*>(A);
+    const TA* b = static_cast<const TA*>(B);
+    if (epi == EPI_STORE)
+      k_gemm_simt<TA, EPI_STORE><<<grid, 256, 0, st>>>(Mp, Nn, Kk, a, lda, gA, b, bias, out, ldo,
+                                                       resid, ldr, gR);
+    else if (epi == EPI_GELU)
+      k_gemm_simt<TA, EPI_GELU><<<grid, 256, 0, st>>>(Mp, Nn, Kk, a, lda, gA, b, bias, out, ldo,
+                                                      resid, ldr, gR);
+    else
+      k_gemm_simt<TA, EPI_RESID><<<grid, 256, 0, st>>>(Mp, Nn, Kk, a, lda, gA, b, bias, out, ldo,
+                                                       resid, ldr, gR);
+    ++launches;
+  }
+
+  template <typename TA>
+  void run_chunk(const uint8_t* d_cfg, int S, double* d_e, double* d_logpsi, cudaStream_t st,
+                 std::vector<int32_t>& hK, std::vector<int32_t>& hU, Engine::Taps* taps,
+                 std::vector<int32_t>* tap_codes, std::vector<int64_t>* tap_act_off,
+                 std::vector<int32_t>* tap_t1, std::vector<int64_t>* tap_aoff,
+                 std::vector<double>* tap_lp) {
+    const int R1 = nb + 1;
+    const int64_t R = int64_t(S) * R1;
+    K_.ensure(S); attw_.ensure(S); Mact_.ensure(S); diag_.ensure(S); act_off_.ensure(S); tab_off_.ensure(S);
+    row_bond_.ensure(R); row_t1_.ensure(R); row_aoff_.ensure(R); tok0_.ensure(int64_t(S) * T);
+    Ucnt_.ensure(int64_t(L + 1) * S); Uoff_.ensure(int64_t(L + 1) * S); tot_.ensure(2 * (L + 2));
+    int64_t* tot = tot_.p;  // [0] M total, [1] table total, [2+b] U_b total
+    k_connected<<<(S * 32 + 127) / 128, 128, 0, st>>>(S, N, g, T, nb, d_cfg, d_bonds, K_.p, diag_.p,
+                                                      row_bond_.p, row_t1_.p, row_aoff_.p, Mact_.p,
+                                                      tok0_.p, attw_.p);
+    k_scan<<<1, 1024, 0, st>>>(S, Mact_.p, act_off_.p, tot + 0, 0);
+    k_scan<<<1, 1024, 0, st>>>(S, Mact_.p, tab_off_.p, tot + 1, 1);
+    launches += 3;
+    int64_t totals[2];
+    CK(cudaMemcpyAsync(totals, tot, sizeof(totals), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t M = totals[0], TB = totals[1];
+    // arena
+    lrow_.ensure(M); lpos_.ensure(M); I_a.ensure(M); I_b.ensure(M); code_.ensure(M);
+    slot_.ensure(M); rep_of_.ensure(M); g_code_.ensure(M); g_res_.ensure(M); upos_.ensure(M);
+    if (tkey_.n < size_t(TB)) {
+      tkey_.ensure(TB); trep_.ensure(TB); tuid_.ensure(TB);
+      CK(cudaMemsetAsync(tkey_.p, 0xFF, tkey_.n * sizeof(unsigned long long), st));
+      CK(cudaMemsetAsync(trep_.p, 0x7F, trep_.n * sizeof(int32_t), st));
+    }
+    x_a.ensure(M * d); x_b.ensure(M * d); y_.ensure(M * d);
+    h_.ensure(M * d * esz()); qkv_.ensure(M * 3 * d * esz()); f1_.ensure(M * 4 * d * esz());
+    if (!use_tc) att_.ensure(M * d);
+    lpV_.ensure(M * V);
+    const int64_t Rtot = R * T;
+    k_enumerate<<<int((Rtot + 255) / 256), 256, 0, st>>>(S, R1, T, K_.p, row_t1_.p, row_aoff_.p,
+                                                         act_off_.p, lrow_.p, lpos_.p);
+    // (d) input layer
+    int32_t* Icur = I_a.p;
+    int32_t* Inext = I_b.p;
+    k_dedup<0><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
+                                  slot_.p, lrow_.p, lpos_.p, tok0_.p, row_bond_.p, d_bonds, R1, T,
+                                  g, V, nullptr, nullptr, Icur, rep_of_.p, Ucnt_.p);
+    k_scan<<<1, 1024, 0, st>>>(S, Ucnt_.p, Uoff_.p, tot + 2, 0);
+    k_embed<<<S, 256, 0, st>>>(d, R1, T, g, V, Ucnt_.p, Uoff_.p, act_off_.p, rep_of_.p, lrow_.p,
+                               lpos_.p, tok0_.p, row_bond_.p, d_bonds, tok_embed, pos_embed, x_a.p);
+    launches += 4;
+    float* xcur = x_a.p;
+    float* xnext = x_b.p;
+    const int lnGrid = sms * 8;
+    const float scale = float(1.0 / std::sqrt(double(dh)));
+    for (int b = 0; b < L; ++b) {
+      const DevBlock& B = blk[b];
+      const int64_t* Mb = tot + 2 + b;
+      int32_t* Uc_cur = Ucnt_.p + int64_t(b) * S;
+      int64_t* Uo_cur = Uoff_.p + int64_t(b) * S;
+      int32_t* Uc_next = Ucnt_.p + int64_t(b + 1) * S;
+      int64_t* Uo_next = Uoff_.p + int64_t(b + 1) * S;
+      (void)Uc_cur;
+      TA* h = reinterpret_cast<TA*>(h_.p);
+      TA* qkv = reinterpret_cast<TA*>(qkv_.p);
+      TA* f1 = reinterpret_cast<TA*>(f1_.p);
+      k_layernorm<TA><<<lnGrid, 256, 0, st>>>(Mb, d, xcur, B.ln1_g, B.ln1_b, h);
+      ++launches;
+      gemm<TA>(Mb, M, 3 * d, d, h, d, nullptr, B.wqkv, B.wqkvT, B.bqkv, qkv, 3 * d, EPI_STORE,
+               nullptr, 0, nullptr, st);
+      CK(cudaEventRecord(ev[0], st));
+      if (use_tc) {
+        // fused gathered attention -> codebook distances -> certified argmin
+        tc_attention_vq(S, R1, T, d, dh, nh, Q, scale, K_.p, row_t1_.p, row_aoff_.p, act_off_.p,
+                        Icur, Uo_cur, qkv, B.cbA, B.cb32, code_.p, st, sms, prof);
+        launches += 1;
+      } else {
+        const size_t asmem = (size_t(T) * (dh + 1) + size_t(T) * dh + 4 * T + 4 * dh) * 4;
+        if (asmem > 48 * 1024)
+          CK(cudaFuncSetAttribute(k_attention<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(asmem)));
+        k_attention<TA><<<dim3(unsigned(R), nh), 128, asmem, st>>>(
+            R1, T, d, dh, scale, K_.p, row_t1_.p, row_aoff_.p, act_off_.p, Icur, Uo_cur, qkv,
+            att_.p);
+        CK(cudaEventRecord(ev[2], st));
+        const int LOCS = d > 384 ? 32 : 64;
+        const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;
+        const int vgrid = int(std::max<int64_t>(1, std::min<int64_t>((M + LOCS - 1) / LOCS, sms * 4)));
+        if (LOCS == 64) {
+          if (vsmem > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_vq<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(vsmem)));
+          k_vq<64><<<vgrid, 256, vsmem, st>>>(tot + 0, d, att_.p, B.cb32, Q, code_.p);
+        } else {
+          if (vsmem > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_vq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(vsmem)));
+          k_vq<32><<<vgrid, 256, vsmem, st>>>(tot + 0, d, att_.p, B.cb32, Q, code_.p);
+        }
+        launches += 2;
+      }
+      CK(cudaEventRecord(ev[1], st));
+      {
+        // per-layer stage timing (the engine syncs per chunk anyway)
+        CK(cudaEventSynchronize(ev[1]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        prof[0] += ms;
+        prof[2] += use_tc ? 1 : 2;
+        if (!use_tc) {
+          float ma = 0.f;
+          CK(cudaEventElapsedTime(&ma, ev[0], ev[2]));
+          prof[7] += ma;
+          prof[6] += ms - ma;
+        }
+      }
+      if (tap_codes) {
+        taps_codes_.ensure(M);
+        std::vector<int32_t> hc(M);
+        CK(cudaMemcpyAsync(hc.data(), code_.p, M * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        tap_codes->insert(tap_codes->end(), hc.begin(), hc.end());
+      }
+      k_dedup<1><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
+                                    slot_.p, nullptr, nullptr, nullptr, nullptr, nullptr, R1, T, g,
+                                    V, Icur, code_.p, Inext, rep_of_.p, Uc_next);
+      k_scan<<<1, 1024, 0, st>>>(S, Uc_next, Uo_next, tot + 3 + b, 0);
+      k_build_gather<<<S, 256, 0, st>>>(Uc_next, Uo_next, Uo_cur, act_off_.p, rep_of_.p, code_.p,
+                                        Icur, lpos_.p, g_code_.p, g_res_.p, upos_.p);
+      launches += 3;
+      const int64_t* Mn = tot + 3 + b;
+      // continuation (proj/src/dedup.cpp:246-267): y = r + (code_row Wo + bo)
+      gemm<TA>(Mn, M, d, d, B.cbA, d, g_code_.p, B.wo, B.woT, B.bo, y_.p, d, EPI_RESID, xcur, d,
+               g_res_.p, st);
+      k_layernorm<TA><<<lnGrid, 256, 0, st>>>(Mn, d, y_.p, B.ln2_g, B.ln2_b, h);
+      ++launches;
+      gemm<TA>(Mn, M, 4 * d, d, h, d, nullptr, B.w1, B.w1T, B.b1, f1, 4 * d, EPI_GELU, nullptr, 0,
+               nullptr, st);
+      gemm<TA>(Mn, M, d, 4 * d, f1, 4 * d, nullptr, B.w2, B.w2T, B.b2, xnext, d, EPI_RESID, y_.p, d,
+               nullptr, st);
+      std::swap(xcur, xnext);
+      std::swap(Icur, Inext);
+    }
+    // (e) head and E_loc
+    const int64_t* ML = tot + 2 + L;
+    TA* h = reinterpret_cast<TA*>(h_.p);
+    k_layernorm<TA><<<lnGrid, 256, 0, st>>>(ML, d, xcur, lnf_g, lnf_b, h);
+    k_head<TA><<<lnGrid, 256, 0, st>>>(ML, d, V, lastV, T, h, static_cast<const TA*>(head_w),
+                                       head_b, upos_.p, lpV_.p);
+    double* lp_rows = nullptr;
+    if (tap_lp) {
+      lp_rows_.ensure(R);
+      lp_rows = lp_rows_.p;
+    }
+    k_eloc<<<(S * 32 + 127) / 128, 128, 0, st>>>(S, R1, T, g, V, marshall ? -0.5 : 0.5, K_.p,
+                                                 diag_.p, row_bond_.p, row_t1_.p, row_aoff_.p,
+                                                 act_off_.p, tok0_.p, d_bonds, Icur,
+                                                 Uoff_.p + int64_t(L) * S, lpV_.p, d_e, d_logpsi,
+                                                 lp_rows);
+    launches += 3;
+    CK(cudaGetLastError());
+    hK.resize(S);
+    hU.resize(size_t(L + 1) * S);
+    std::vector<int64_t> haw(S);
+    CK(cudaMemcpyAsync(haw.data(), attw_.p, S * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hK.data(), K_.p, S * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hU.data(), Ucnt_.p, hU.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (taps) {
+      tap_act_off->resize(S);
+      tap_t1->resize(R);
+      tap_aoff->resize(R);
+      CK(cudaMemcpyAsync(tap_act_off->data(), act_off_.p, S * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(tap_t1->data(), row_t1_.p, R * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(tap_aoff->data(), row_aoff_.p, R * 8, cudaMemcpyDeviceToHost, st));
+      tap_lp->resize(R);
+      CK(cudaMemcpyAsync(tap_lp->data(), lp_rows_.p, R * 8, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    // algorithmic work of the attention->VQ stage actually executed
+    double aw = 0;
+    for (int s2 = 0; s2 < S; ++s2) aw += double(haw[s2]);
+    prof[1] += double(L) * (4.0 * d * aw + 2.0 * double(d) * Q * double(M));
+    prof[3] += double(M) * L;
+    for (int s2 = 0; s2 < S; ++s2)
+      for (int b = 0; b < L; ++b) {
+        prof[4] += hU[size_t(b) * S + s2];
+        prof[5] += hU[size_t(b + 1) * S + s2];
+      }
+  }
+
+  void run_device(const uint8_t* d_cfg, int64_t B, double* d_e, double* d_logpsi, int64_t* ledger7,
+                  cudaStream_t st, Engine::Taps* taps) {
+    if (!d_bonds && nb == 0 && h_bonds.empty())
+      throw UsageError("set_hamiltonian must be called before local_energies");
+    CK(cudaSetDevice(dev));
+    launches = 0;
+    for (double& v : prof) v = 0;
+    if (!ev[0])
+      for (auto& e : ev) CK(cudaEventCreate(&e));
+    int64_t tap_code_pos = 0, tap_lp_pos = 0;
+    for (int64_t s0 = 0; s0 < B; s0 += S_max) {
+      const int S = int(std::min<int64_t>(S_max, B - s0));
+      std::vector<int32_t> hK, hU;
+      std::vector<int32_t> tcodes;
+      std::vector<int64_t> tact, taoff;
+      std::vector<int32_t> tt1;
+      std::vector<double> tlp;
+      if (prec == VQNQS_PREC_BF16)
+        run_chunk<bf16>(d_cfg + s0 * N, S, d_e + s0, d_logpsi + s0, st, hK, hU, taps,
+                        taps ? &tcodes : nullptr, &tact, &tt1, &taoff, taps ? &tlp : nullptr);
+      else
+        run_chunk<float>(d_cfg + s0 * N, S, d_e + s0, d_logpsi + s0, st, hK, hU, taps,
+                         taps ? &tcodes : nullptr, &tact, &tt1, &taoff, taps ? &tlp : nullptr);
+      for (int s = 0; s < S; ++s) {
+        std::vector<int64_t> U(L + 1);
+        for (int b = 0; b <= L; ++b) U[b] = hU[size_t(b) * S + s];
+        if (ledger7) ledger_add(c, hK[s], U.data(), ledger7);
+        if (taps) {
+          if (taps->K) taps->K[s0 + s] = hK[s];
+          if (taps->U)
+            for (int b = 0; b <= L; ++b) taps->U[(s0 + s) * (L + 1) + b] = U[b];
+        }
+      }
+      if (taps) {
+        const int R1 = nb + 1;
+        const int64_t M = int64_t(tcodes.size()) / std::max(1, L);
+        for (int s = 0; s < S; ++s) {
+          const int Ks = hK[s];
+          if (taps->codes) {
+            if (tap_code_pos + int64_t(L) * Ks * T > taps->codes_cap)
+              throw ShapeError("taps: codes buffer too small");
+            for (int b = 0; b < L; ++b)
+              for (int k = 0; k < Ks; ++k) {
+                const int64_t r = int64_t(s) * R1 + k;
+                const int a = k == 0 ? 0 : tt1[r] + 1;
+                for (int p = 0; p < T; ++p) {
+                  const int64_t loc = p < a ? tact[s] + p : tact[s] + taoff[r] + (p - a);
+                  taps->codes[tap_code_pos + (int64_t(b) * Ks + k) * T + p] =
+                      tcodes[size_t(b) * M + loc];
+                }
+              }
+            tap_code_pos += int64_t(L) * Ks * T;
+          }
+          if (taps->lp_rows) {
+            if (tap_lp_pos + Ks > taps->lp_cap) throw ShapeError("taps: lp buffer too small");
+            for (int k = 0; k < Ks; ++k) taps->lp_rows[tap_lp_pos + k] = tlp[int64_t(s) * R1 + k];
+            tap_lp_pos += Ks;
+          }
+        }
+      }
+    }
+  }
+
+  void run_host(const uint8_t* configs, int64_t B, double* e_re, double* e_im, double* logpsi,
+                int64_t* ledger7, Engine::Taps* taps) {
+    CK(cudaSetDevice(dev));
+    const size_t nbytes = size_t(B) * N;
+    if (h_pinned_cfg_n < nbytes) {
+      if (h_pinned_cfg) cudaFreeHost(h_pinned_cfg);
+      CK(cudaMallocHost(&h_pinned_cfg, nbytes));
+      h_pinned_cfg_n = nbytes;
+    }
+    if (h_pinned_out_n < size_t(2 * B)) {
+      if (h_pinned_out) cudaFreeHost(h_pinned_out);
+      CK(cudaMallocHost(&h_pinned_out, 2 * B * sizeof(double)));
+      h_pinned_out_n = 2 * B;
+    }
+    std::memcpy(h_pinned_cfg, configs, nbytes);
+    cfg_stage_.ensure(nbytes);
+    out_stage_.ensure(2 * B);
+    CK(cudaMemcpyAsync(cfg_stage_.p, h_pinned_cfg, nbytes, cudaMemcpyHostToDevice, own));
+    run_device(cfg_stage_.p, B, out_stage_.p, out_stage_.p + B, ledger7, own, taps);
+    CK(cudaMemcpyAsync(h_pinned_out, out_stage_.p, 2 * B * sizeof(double), cudaMemcpyDeviceToHost,
+                       own));
+    CK(cudaStreamSynchronize(own));
+    for (int64_t i = 0; i < B; ++i) {
+      const double e = h_pinned_out[i];
+      if (!std::isfinite(e)) {
+        std::string s;
+        for (int j = 0; j < N; ++j) s.push_back(configs[i * N + j] ? '1' : '0');
+        throw NumericError("non-finite local energy at configuration " + s);
+      }
+      e_re[i] = e;
+      if (e_im) e_im[i] = 0.0;
+      if (logpsi) logpsi[i] = h_pinned_out[B + i];
+    }
+  }
+};
+
+Engine::Engine(const vqnqs_model_desc& d, const double* const* params, int n_params, int precision,
+               int device)
+    : p_(new EngineImpl(d, params, n_params, precision, device)) {}
+Engine::~Engine() { delete p_; }
+void Engine::set_hamiltonian(const int32_t* bonds, int nb, int n_sites, bool marshall) {
+  p_->set_hamiltonian(bonds, nb, n_sites, marshall);
+}
+void Engine::run_device(const uint8_t* d_configs, int64_t B, double* d_e, double* d_logpsi,
+                        int64_t* ledger7, void* stream, Taps* taps) {
+  p_->run_device(d_configs, B, d_e, d_logpsi, ledger7,
+                 stream ? static_cast<cudaStream_t>(stream) : p_->own, taps);
+}
+void Engine::run_host(const uint8_t* configs, int64_t B, double* e_re, double* e_im,
+                      double* logpsi, int64_t* ledger7, Taps* taps) {
+  p_->run_host(configs, B, e_re, e_im, logpsi, ledger7, taps);
+}
+int64_t Engine::last_launches() const { return p_->launches; }
+int Engine::last_profile(double* out, int cap) const {
+  for (int i = 0; i < cap && i < 8; ++i) out[i] = p_->prof[i];
+  return 8;
+}
+const vqnqs_model_desc& Engine::desc() const { return p_->c; }
+
+}  // namespace vqb

@@ -1,0 +1,428 @@
+// Integer / byte-bound stages of the local-energy pipeline:
+//   (a) connected configurations          k_connected, k_enumerate
+//   (d) unique-row dedup + gather build   k_dedup, k_build_gather, k_embed
+//   (e) head + segmented E_loc reduction  k_head, k_eloc
+// plus per-sample scans and the LayerNorm row kernel.
+//
+// Row/location layout. A micro-batch holds S samples. Rows of
+// sample s (its connected set, proj/src/hamiltonian.cpp:41-74) live at fixed
+// capacity slots r = s*R1 + k, R1 = n_bonds + 1, k = 0 the diagonal row. Row
+// k >= 1 flips bond row_bond[r]; t1 = its first changed token position. A
+// location (k, p) is ACTIVE when its hidden state can differ from the base
+// row's: p >= a_k = t1 + 1 (a_0 = 0). Inactive locations provably carry the
+// base row's state at every layer (causal attention, identical inputs), so
+// they are never stored: they map to the base location (0, p). Active
+// locations of a sample are compact from act_off[s]: the base row's T
+// locations first, then each row's suffix in row order.
+#pragma once
+
+#include "common.cuh"
+
+namespace vqb {
+
+// Target token at position p of row r (little-endian groups of g spins,
+// proj/src/model.cpp:236-248): base token with the flipped bond's bits toggled.
+__device__ __forceinline__ int row_token(const int32_t* tok0, const int32_t* bonds, int bond,
+                                         int g, int p) {
+  int t = tok0[p];
+  if (bond >= 0) {
+    const int i = bonds[2 * bond], j = bonds[2 * bond + 1];
+    if (i / g == p) t ^= 1 << (i % g);
+    if (j / g == p) t ^= 1 << (j % g);
+  }
+  return t;
+}
+
+// ---------------------------------------------------------------- (a)
+// connected_set (proj/src/hamiltonian.cpp:41-74), one warp per sample:
+// diagonal 1/4 sum z_i z_j (exact in double: multiples of 1/4), and one row
+// per antiparallel bond in bond order (ballot + popc keeps the order).
+__global__ void k_connected(int S, int N, int g, int T, int nb, const uint8_t* __restrict__ cfg,
+                            const int32_t* __restrict__ bonds, int32_t* __restrict__ K,
+                            double* __restrict__ diag, int32_t* __restrict__ row_bond,
+                            int32_t* __restrict__ row_t1, int64_t* __restrict__ row_aoff,
+                            int32_t* __restrict__ Mact, int32_t* __restrict__ tok0,
+                            int64_t* __restrict__ attw) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= S) return;
+  const int s = warp;
+  const uint8_t* c = cfg + (int64_t)s * N;
+  const int R1 = nb + 1;
+  for (int p = lane; p < T; p += 32) {
+    int t = 0;
+    for (int j = 0; j < g; ++j)
+      if (p * g + j < N) t |= int(c[p * g + j] & 1) << j;
+    tok0[(int64_t)s * T + p] = t;
+  }
+  int zz = 0;
+  int nrows = 1;
+  int64_t aoff = T;  // base row's T locations come first
+  // sum over active locations of (p + 1): the causal attention work
+  int64_t aw = (int64_t)T * (T + 1) / 2;
+  if (lane == 0) {
+    row_bond[(int64_t)s * R1] = -1;
+    row_t1[(int64_t)s * R1] = -1;
+    row_aoff[(int64_t)s * R1] = 0;
+  }
+  for (int b0 = 0; b0 < nb; b0 += 32) {
+    const int b = b0 + lane;
+    bool anti = false;
+    int cnt = 0, t1 = 0;
+    if (b < nb) {
+      const int i = bonds[2 * b], j = bonds[2 * b + 1];
+      const int zi = 2 * int(c[i]) - 1, zj = 2 * int(c[j]) - 1;
+      zz += zi * zj;
+      anti = c[i] != c[j];
+      t1 = min(i / g, j / g);
+      cnt = T - (t1 + 1);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, anti);
+    const int before = __popc(m & ((1u << lane) - 1u));
+    // inclusive scan of active counts among anti lanes
+    int v = anti ? cnt : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += n;
+    }
+    if (anti) {
+      const int64_t r = (int64_t)s * R1 + nrows + before;
+      row_bond[r] = b;
+      row_t1[r] = t1;
+      row_aoff[r] = aoff + v - cnt;
+    }
+    nrows += __popc(m);
+    aoff += __shfl_sync(0xffffffffu, v, 31);
+    int64_t w = anti ? ((int64_t)T * (T + 1) / 2 - (int64_t)(t1 + 1) * (t1 + 2) / 2) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    aw += w;
+  }
+  zz = warp_sum_i(zz);
+  if (lane == 0) {
+    K[s] = nrows;
+    diag[s] = 0.25 * (double)zz;
+    Mact[s] = (int32_t)aoff;
+    attw[s] = aw;
+  }
+}
+
+// Exclusive scan of per-sample counts (single CTA). mode 1 scans hash-table
+// capacities (next power of two >= 2*count + 2) instead of the counts.
+__global__ void k_scan(int n, const int32_t* __restrict__ in, int64_t* __restrict__ off,
+                       int64_t* __restrict__ total, int mode) {
+  __shared__ int64_t wsum[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (n + nt - 1) / nt;
+  const int b = tid * per, e = min(n, b + per);
+  auto val = [&](int i) -> int64_t {
+    int64_t v = in[i];
+    if (mode == 1) {
+      int64_t c = 16;
+      while (c < 2 * v + 2) c <<= 1;
+      v = c;
+    }
+    return v;
+  };
+  int64_t loc = 0;
+  for (int i = b; i < e; ++i) loc += val(i);
+  // block exclusive scan of loc
+  int64_t x = loc;
+  const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t y = lane < (nt >> 5) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t z = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += z;
+    }
+    wsum[lane] = y;
+  }
+  __syncthreads();
+  int64_t run = x - loc + (w > 0 ? wsum[w - 1] : 0);
+  for (int i = b; i < e; ++i) {
+    off[i] = run;
+    run += val(i);
+  }
+  if (tid == nt - 1) *total = run;
+}
+
+// Location -> (row slot, position) for every active location.
+__global__ void k_enumerate(int S, int R1, int T, const int32_t* __restrict__ K,
+                            const int32_t* __restrict__ row_t1,
+                            const int64_t* __restrict__ row_aoff,
+                            const int64_t* __restrict__ act_off, int32_t* __restrict__ lrow,
+                            int16_t* __restrict__ lpos) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = idx / T;
+  const int p = int(idx % T);
+  if (r >= (int64_t)S * R1) return;
+  const int s = int(r / R1), k = int(r % R1);
+  if (k >= K[s]) return;
+  const int a = k == 0 ? 0 : row_t1[r] + 1;
+  if (p < a) return;
+  const int64_t loc = act_off[s] + row_aoff[r] + (p - a);
+  lrow[loc] = int32_t(r);
+  lpos[loc] = int16_t(p);
+}
+
+// ---------------------------------------------------------------- (d)
+// Exact-key unique rows of one sample's active locations, numbered in first
+// occurrence order exactly like the reference's unordered_map emplace loops
+// (compress_inputs, proj/src/dedup.cpp:52-76; requantize, :151-175).
+//   MODE 0 (input layer): key = (p, BOS-shifted token)      dedup.cpp:61-63
+//   MODE 1 (after VQ):    key = (residual row, VQ code)     dedup.cpp:156-159
+// One CTA per sample; open-addressing table in global memory (L2-resident),
+// atomicCAS claims a slot, atomicMin keeps the first location, a block scan
+// over locations in order assigns ids. Slots are reset before exit so the
+// table is clean for the next layer.
+template <int MODE>
+__global__ void __launch_bounds__(512) k_dedup(
+    const int32_t* __restrict__ Mact, const int64_t* __restrict__ act_off,
+    const int64_t* __restrict__ tab_off, unsigned long long* __restrict__ tkey,
+    int32_t* __restrict__ trep, int32_t* __restrict__ tuid, int32_t* __restrict__ slot,
+    // MODE 0 inputs
+    const int32_t* __restrict__ lrow, const int16_t* __restrict__ lpos,
+    const int32_t* __restrict__ tok0, const int32_t* __restrict__ row_bond,
+    const int32_t* __restrict__ bonds, int R1, int T, int g, int V,
+    // MODE 1 inputs
+    const int32_t* __restrict__ I_in, const int32_t* __restrict__ code,
+    // outputs
+    int32_t* __restrict__ I_out, int32_t* __restrict__ rep_of, int32_t* __restrict__ Ucnt) {
+  __shared__ int wtot[32];
+  __shared__ int run_s;
+  const int s = blockIdx.x;
+  const int M = Mact[s];
+  const int64_t base = act_off[s];
+  const int64_t tb = tab_off[s];
+  int64_t cap = 16;
+  while (cap < 2 * (int64_t)M + 2) cap <<= 1;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
+  // phase 1: insert
+  for (int i = tid; i < M; i += nt) {
+    const int64_t loc = base + i;
+    unsigned long long key;
+    if (MODE == 0) {
+      const int r = lrow[loc];
+      const int p = lpos[loc];
+      const int sidx = r / R1;
+      const int tok = p == 0 ? V : row_token(tok0 + (int64_t)sidx * T, bonds, row_bond[r], g, p - 1);
+      key = (unsigned long long)p * (unsigned long long)(V + 1) + (unsigned long long)tok;
+    } else {
+      key = ((unsigned long long)(uint32_t)I_in[loc] << 32) | (uint32_t)code[loc];
+    }
+    int64_t h = (int64_t)(hash64(key) & (uint64_t)(cap - 1));
+    for (;;) {
+      const unsigned long long prev = atomicCAS(&tkey[tb + h], VQB_EMPTY_KEY, key);
+      if (prev == VQB_EMPTY_KEY || prev == key) {
+        atomicMin(&trep[tb + h], i);
+        slot[loc] = (int32_t)h;
+        break;
+      }
+      h = (h + 1) & (cap - 1);
+    }
+  }
+  if (tid == 0) run_s = 0;
+  __syncthreads();
+  // phase 2: ids in first-occurrence order
+  for (int c0 = 0; c0 < M; c0 += nt) {
+    const int i = c0 + tid;
+    bool flag = false;
+    int64_t h = 0;
+    if (i < M) {
+      h = slot[base + i];
+      flag = trep[tb + h] == i;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, flag);
+    const int before = __popc(m & ((1u << lane) - 1u));
+    if (lane == 0) wtot[w] = __popc(m);
+    __syncthreads();
+    if (w == 0) {
+      int v = lane < (nt >> 5) ? wtot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      wtot[lane] = v;  // inclusive
+    }
+    __syncthreads();
+    const int run = run_s;
+    if (flag) {
+      const int id = run + (w > 0 ? wtot[w - 1] : 0) + before;
+      tuid[tb + h] = id;
+      rep_of[base + id] = i;
+    }
+    __syncthreads();
+    if (tid == 0) run_s = run + wtot[(nt >> 5) - 1];
+    __syncthreads();
+  }
+  // phase 3: scatter ids to locations
+  for (int i = tid; i < M; i += nt) I_out[base + i] = tuid[tb + slot[base + i]];
+  if (tid == 0) Ucnt[s] = run_s;
+  __syncthreads();
+  // phase 4: reset touched slots
+  for (int i = tid; i < M; i += nt) {
+    const int64_t h = slot[base + i];
+    tkey[tb + h] = VQB_EMPTY_KEY;
+    trep[tb + h] = VQB_INT_MAX;
+  }
+}
+
+// Input embeddings of the unique input rows: tok_embed[tok] + pos_embed[p]
+// (proj/src/dedup.cpp:79-89).
+__global__ void k_embed(int d, int R1, int T, int g, int V, const int32_t* __restrict__ Ucnt,
+                        const int64_t* __restrict__ Uoff, const int64_t* __restrict__ act_off,
+                        const int32_t* __restrict__ rep_of, const int32_t* __restrict__ lrow,
+                        const int16_t* __restrict__ lpos, const int32_t* __restrict__ tok0,
+                        const int32_t* __restrict__ row_bond, const int32_t* __restrict__ bonds,
+                        const float* __restrict__ tok_embed, const float* __restrict__ pos_embed,
+                        float* __restrict__ x) {
+  const int s = blockIdx.x;
+  const int U = Ucnt[s];
+  const int64_t base = act_off[s];
+  for (int64_t idx = threadIdx.x; idx < (int64_t)U * d; idx += blockDim.x) {
+    const int uid = int(idx / d), c = int(idx % d);
+    const int64_t loc = base + rep_of[base + uid];
+    const int r = lrow[loc], p = lpos[loc];
+    const int tok = p == 0 ? V : row_token(tok0 + (int64_t)s * T, bonds, row_bond[r], g, p - 1);
+    x[(Uoff[s] + uid) * d + c] = tok_embed[(int64_t)tok * d + c] + pos_embed[(int64_t)p * d + c];
+  }
+}
+
+// kernels::layer_norm (proj/src/tensor.cpp:57-83): two-pass biased variance,
+// eps 1e-5, statistics in double; one warp per row over *Mp rows.
+template <typename TA>
+__global__ void k_layernorm(const int64_t* __restrict__ Mp, int d, const float* __restrict__ x,
+                            const float* __restrict__ gam, const float* __restrict__ bet,
+                            TA* __restrict__ out) {
+  const int64_t M = *Mp;
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
+    const float* xr = x + r * d;
+    double s = 0.0;
+    for (int c = lane; c < d; c += 32) s += xr[c];
+    const double mean = warp_sum(s) / d;
+    double v = 0.0;
+    for (int c = lane; c < d; c += 32) {
+      const double t = xr[c] - mean;
+      v += t * t;
+    }
+    const double var = warp_sum(v) / d;
+    const double rstd = 1.0 / sqrt(var + 1e-5);
+    for (int c = lane; c < d; c += 32)
+      out[r * d + c] = from_f<TA>((float)((xr[c] - mean) * rstd * gam[c] + bet[c]));
+  }
+}
+
+// For each new unique row (global id g): which codebook row and which
+// residual row it concatenates (requantize's V' = [code row || residual row],
+// proj/src/dedup.cpp:176-184), and its token position.
+__global__ void k_build_gather(const int32_t* __restrict__ Ucnt_next,
+                               const int64_t* __restrict__ Uoff_next,
+                               const int64_t* __restrict__ Uoff_cur,
+                               const int64_t* __restrict__ act_off,
+                               const int32_t* __restrict__ rep_of,
+                               const int32_t* __restrict__ code, const int32_t* __restrict__ I_cur,
+                               const int16_t* __restrict__ lpos, int32_t* __restrict__ g_code,
+                               int64_t* __restrict__ g_res, int16_t* __restrict__ upos) {
+  const int s = blockIdx.x;
+  const int U = Ucnt_next[s];
+  const int64_t base = act_off[s];
+  for (int uid = threadIdx.x; uid < U; uid += blockDim.x) {
+    const int64_t loc = base + rep_of[base + uid];
+    const int64_t gi = Uoff_next[s] + uid;
+    g_code[gi] = code[loc];
+    g_res[gi] = Uoff_cur[s] + I_cur[loc];
+    upos[gi] = lpos[loc];
+  }
+}
+
+// ---------------------------------------------------------------- (e)
+// LN_f output -> head linear -> (pad mask) -> log_softmax in double
+// (proj/src/dedup.cpp:284-308, tensor.cpp:107-124). One warp per unique row.
+template <typename TA>
+__global__ void k_head(const int64_t* __restrict__ Mp, int d, int V, int lastV, int T,
+                       const TA* __restrict__ h, const TA* __restrict__ W,
+                       const float* __restrict__ b, const int16_t* __restrict__ upos,
+                       double* __restrict__ lpV) {
+  const int64_t M = *Mp;
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  double logit[16];
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
+    for (int c = 0; c < V; ++c) {
+      float acc = 0.f;
+      for (int e = lane; e < d; e += 32) acc += to_f<TA>(h[r * d + e]) * to_f<TA>(W[(int64_t)e * V + c]);
+      acc = warp_sum(acc);
+      logit[c] = (double)(acc + b[c]);
+      if (lastV < V && c >= lastV && upos[r] == T - 1) logit[c] = -1e30;
+    }
+    double mx = logit[0];
+    for (int c = 1; c < V; ++c) mx = fmax(mx, logit[c]);
+    double sum = 0.0;
+    for (int c = 0; c < V; ++c) sum += exp(logit[c] - mx);
+    const double lse = mx + log(sum);
+    if (lane < V) {
+      double v = 0.0;
+      for (int c = 0; c < V; ++c)
+        if (c == lane) v = logit[c] - lse;
+      lpV[r * V + lane] = v;
+    }
+  }
+}
+
+// Segmented psi-ratio sum, one warp per sample (proj/src/dedup.cpp:310-321,
+// 410-417). lp_k - lp_0 is accumulated only over positions p >= t1_k, where
+// row k's target token or hidden state can differ from the base row's; the
+// shared prefix cancels exactly. E = diag + sum_{k>=1} c * exp(0.5 (lp_k - lp_0)).
+__global__ void k_eloc(int S, int R1, int T, int g, int V, double coeff,
+                       const int32_t* __restrict__ K, const double* __restrict__ diag,
+                       const int32_t* __restrict__ row_bond, const int32_t* __restrict__ row_t1,
+                       const int64_t* __restrict__ row_aoff, const int64_t* __restrict__ act_off,
+                       const int32_t* __restrict__ tok0, const int32_t* __restrict__ bonds,
+                       const int32_t* __restrict__ I_L, const int64_t* __restrict__ Uoff_L,
+                       const double* __restrict__ lpV, double* __restrict__ e_out,
+                       double* __restrict__ logpsi, double* __restrict__ lp_rows) {
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= S) return;
+  const int32_t* t0 = tok0 + (int64_t)s * T;
+  const int64_t base = act_off[s];
+  const int64_t uo = Uoff_L[s];
+  double lp0 = 0.0;
+  for (int p = lane; p < T; p += 32) lp0 += lpV[(uo + I_L[base + p]) * V + t0[p]];
+  lp0 = warp_sum(lp0);
+  const int Ks = K[s];
+  double acc = 0.0;
+  for (int k = 1 + lane; k < Ks; k += 32) {
+    const int64_t r = (int64_t)s * R1 + k;
+    const int bond = row_bond[r], t1 = row_t1[r], a = t1 + 1;
+    const int64_t rloc = base + row_aoff[r];
+    double diff = 0.0;
+    for (int p = t1; p < T; ++p) {
+      const int64_t u0 = uo + I_L[base + p];
+      const int64_t uk = p < a ? u0 : uo + I_L[rloc + (p - a)];
+      diff += lpV[uk * V + row_token(t0, bonds, bond, g, p)] - lpV[u0 * V + t0[p]];
+    }
+    acc += coeff * exp(0.5 * diff);
+    if (lp_rows) lp_rows[r] = lp0 + diff;
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    e_out[s] = diag[s] + acc;
+    logpsi[s] = 0.5 * lp0;
+    if (lp_rows) lp_rows[(int64_t)s * R1] = lp0;
+  }
+}
+
+}  // namespace vqb

@@ -1,0 +1,227 @@
+// CUDA-core kernels for (b) and (c): the portable correctness path and the
+// fp32 configurations (c1, c2), where tcgen05 has no exact fp32 mode.
+//   k_gemm_simt  per-location linear layers on unique rows, fused epilogues
+//   k_attention  gathered causal multi-head attention over active locations
+//   k_vq         exact fp32 nearest-codeword search (ties -> lowest index)
+#pragma once
+
+#include "common.cuh"
+
+namespace vqb {
+
+enum { EPI_STORE = 0, EPI_GELU = 1, EPI_RESID = 2 };
+
+// C[M x N] = A[M x K] . B[K x N] + bias, B row-major [in x out] like the
+// reference's weights (proj/src/tensor.cpp:43-55). A rows may be gathered
+// (row gA[m]); EPI_RESID adds resid[gR ? gR[m] : m] in fp32 after the bias,
+// matching y = r + (a W + b) (proj/src/dedup.cpp:255-256,262-265).
+// Persistent over 64x64 tiles; M is read from device memory.
+template <typename TA, int EPI>
+__global__ void __launch_bounds__(256) k_gemm_simt(
+    const int64_t* __restrict__ Mp, int N, int K, const TA* __restrict__ A, int lda,
+    const int32_t* __restrict__ gA, const TA* __restrict__ B, const float* __restrict__ bias,
+    void* __restrict__ out, int ldo, const float* __restrict__ resid, int ldr,
+    const int64_t* __restrict__ gR) {
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int64_t M = *Mp;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t tilesM = (M + BM - 1) / BM, tilesN = (N + BN - 1) / BN;
+  for (int64_t tile = blockIdx.x; tile < tilesM * tilesN; tile += gridDim.x) {
+    const int64_t m0 = (tile / tilesN) * BM;
+    const int n0 = int(tile % tilesN) * BN;
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = tid + q * 256;
+        const int r = e >> 4, kk = e & 15;
+        const int64_t m = m0 + r;
+        float v = 0.f;
+        if (m < M) {
+          const int64_t ar = gA ? (int64_t)gA[m] : m;
+          v = to_f<TA>(A[ar * lda + k0 + kk]);
+        }
+        As[kk][r] = v;
+        const int kb = e >> 6, n = e & 63;
+        Bs[kb][n] = (n0 + n < N) ? to_f<TA>(B[(int64_t)(k0 + kb) * N + n0 + n]) : 0.f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        float a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t m = m0 + ty * 4 + i;
+      if (m >= M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = n0 + tx * 4 + j;
+        if (n >= N) continue;
+        const float v = acc[i][j] + bias[n];
+        if (EPI == EPI_STORE) {
+          static_cast<TA*>(out)[m * ldo + n] = from_f<TA>(v);
+        } else if (EPI == EPI_GELU) {
+          static_cast<TA*>(out)[m * ldo + n] = from_f<TA>(gelu_f(v));
+        } else {
+          const int64_t rr = gR ? gR[m] : m;
+          static_cast<float*>(out)[m * ldo + n] = resid[rr * ldr + n] + v;
+        }
+      }
+    }
+  }
+}
+
+// Gathered causal attention for one (row, head): softmax(q k^T / sqrt(dh),
+// causal) v over the row's T positions (proj/src/tensor.cpp:199-231), only
+// for the row's active query positions p >= a. Keys/values at positions
+// t < a are the base row's (they are identical). q/k/v come from the unique
+// QKV table through the location->row index I, never expanded
+// (proj/src/dedup.cpp:31-37,128-134). Probabilities are normalised before
+// the value product and rounded to the operand type like the reference's
+// product operands.
+template <typename TA>
+__global__ void __launch_bounds__(128) k_attention(
+    int R1, int T, int d, int dh, float scale, const int32_t* __restrict__ Ks,
+    const int32_t* __restrict__ row_t1, const int64_t* __restrict__ row_aoff,
+    const int64_t* __restrict__ act_off, const int32_t* __restrict__ I,
+    const int64_t* __restrict__ Uoff, const TA* __restrict__ qkv, float* __restrict__ att) {
+  extern __shared__ float sm[];
+  const int r = blockIdx.x, h = blockIdx.y;
+  const int s = r / R1, k = r % R1;
+  if (k >= Ks[s]) return;
+  const int a = k == 0 ? 0 : row_t1[r] + 1;
+  if (a >= T) return;
+  float* Kt = sm;                    // [T][dh+1]
+  float* Vt = Kt + T * (dh + 1);     // [T][dh]
+  float* P = Vt + T * dh;            // [4][T]
+  float* Qw = P + 4 * T;             // [4][dh]
+  const int64_t base = act_off[s], rloc = base + row_aoff[r], uo = Uoff[s];
+  const int ld = 3 * d;
+  for (int idx = threadIdx.x; idx < T * dh; idx += blockDim.x) {
+    const int t = idx / dh, e = idx % dh;
+    const int64_t loc = t < a ? base + t : rloc + (t - a);
+    const int64_t u = uo + I[loc];
+    Kt[t * (dh + 1) + e] = to_f<TA>(qkv[u * ld + d + h * dh + e]);
+    Vt[t * dh + e] = to_f<TA>(qkv[u * ld + 2 * d + h * dh + e]);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* Pw = P + warp * T;
+  float* q = Qw + warp * dh;
+  for (int p = a + warp; p < T; p += 4) {
+    const int64_t loc = rloc + (p - a);
+    const int64_t u = uo + I[loc];
+    for (int e = lane; e < dh; e += 32) q[e] = to_f<TA>(qkv[u * ld + h * dh + e]);
+    __syncwarp();
+    float mx = -INFINITY;
+    for (int t = lane; t <= p; t += 32) {
+      float sc = 0.f;
+      for (int e = 0; e < dh; ++e) sc = fmaf(q[e], Kt[t * (dh + 1) + e], sc);
+      sc *= scale;
+      Pw[t] = sc;
+      mx = fmaxf(mx, sc);
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int t = lane; t <= p; t += 32) {
+      const float ev = expf(Pw[t] - mx);
+      Pw[t] = ev;
+      sum += ev;
+    }
+    sum = warp_sum(sum);
+    for (int t = lane; t <= p; t += 32) Pw[t] = operand_round<TA>(Pw[t] / sum);
+    __syncwarp();
+    for (int e = lane; e < dh; e += 32) {
+      float o = 0.f;
+      for (int t = 0; t <= p; ++t) o = fmaf(Pw[t], Vt[t * dh + e], o);
+      att[loc * d + h * dh + e] = o;
+    }
+    __syncwarp();
+  }
+}
+
+// Nearest codeword per location (vq_apply_rows, proj/src/model.cpp:283-319,
+// H = 1): argmin_j sum_c (x_c - W_jc)^2 in fp32, ties to the lowest j.
+// LOCS locations per CTA x 32-code chunks staged in shared memory.
+template <int LOCS>
+__global__ void __launch_bounds__(256) k_vq(const int64_t* __restrict__ Mp, int d,
+                                            const float* __restrict__ att,
+                                            const float* __restrict__ cb, int Q,
+                                            int32_t* __restrict__ code) {
+  extern __shared__ float sm[];
+  constexpr int G = 256 / LOCS;  // code groups per chunk
+  constexpr int CH = 32;         // codes per chunk
+  constexpr int PER = CH / G;
+  float* X = sm;                          // [LOCS][d+1]
+  float* W = X + LOCS * (d + 1);          // [CH][d+1]
+  float* rd = W + CH * (d + 1);           // [G][LOCS]
+  int* rj = reinterpret_cast<int*>(rd + G * LOCS);
+  const int64_t M = *Mp;
+  const int tid = threadIdx.x, li = tid % LOCS, jg = tid / LOCS;
+  for (int64_t l0 = (int64_t)blockIdx.x * LOCS; l0 < M; l0 += (int64_t)gridDim.x * LOCS) {
+    for (int idx = tid; idx < LOCS * d; idx += 256) {
+      const int r = idx / d, c = idx % d;
+      X[r * (d + 1) + c] = (l0 + r < M) ? att[(l0 + r) * d + c] : 0.f;
+    }
+    float best = INFINITY;
+    int bj = 0;
+    for (int j0 = 0; j0 < Q; j0 += CH) {
+      __syncthreads();
+      for (int idx = tid; idx < CH * d; idx += 256) {
+        const int j = idx / d, c = idx % d;
+        W[j * (d + 1) + c] = (j0 + j < Q) ? cb[(int64_t)(j0 + j) * d + c] : 0.f;
+      }
+      __syncthreads();
+      for (int jj = jg * PER; jj < jg * PER + PER; ++jj) {
+        if (j0 + jj >= Q) break;
+        const float* xr = X + li * (d + 1);
+        const float* wr = W + jj * (d + 1);
+        float s2 = 0.f;
+        for (int c = 0; c < d; ++c) {
+          const float df = xr[c] - wr[c];
+          s2 = fmaf(df, df, s2);
+        }
+        if (s2 < best) {
+          best = s2;
+          bj = j0 + jj;
+        }
+      }
+    }
+    rd[jg * LOCS + li] = best;
+    rj[jg * LOCS + li] = bj;
+    __syncthreads();
+    if (jg == 0 && l0 + li < M) {
+      float b = rd[li];
+      int j = rj[li];
+      for (int q = 1; q < G; ++q) {
+        const float v = rd[q * LOCS + li];
+        const int vj = rj[q * LOCS + li];
+        if (v < b || (v == b && vj < j)) {
+          b = v;
+          j = vj;
+        }
+      }
+      code[l0 + li] = j;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace vqb

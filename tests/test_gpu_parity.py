@@ -1,0 +1,149 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle (the C
+restatement in oracle/_port, itself pinned bit-for-bit to the reference in
+tests/test_oracle.py) on the same seeded inputs. See tests/parity.py for the
+contract and how near-tie code flips are accounted.
+
+fp32 configs (c1, c2) are checked against the oracle in plain double. bf16
+configs (c3-c5) are checked against the oracle in bf16-emulation mode (both
+operands of every product rounded to bf16, weights snapped to bf16 on both
+sides); their remaining difference is fp32 vs double
+accumulation, which moves codes only at near-ties — BF16_WINDOW bounds it.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2212_11296_b200 as P
+from parity import GAP_FLAG, ParityReport, compare
+
+pytestmark = pytest.mark.gpu
+
+BF16_WINDOW = 1e-4  # documented accumulation window for bf16 configs
+# bf16 operand rounding moves logits by ~2^-9 relative per rounding decision
+# that fp32-vs-double accumulation tips the other way; measured and bounded
+# here. The strict 1e-5 / 1e-4 contract is checked on every
+# config in fp32 mode (test_*_fp32_strict).
+BF16_LOGPSI_TOL = 5e-3
+BF16_ELOC_RTOL = 2e-3
+
+
+def setup(port, name, n_samples, start=0, precision=None):
+    w = P.workload(name)
+    precision = precision or w.precision
+    bf = precision == "bf16"
+    model = P.VqTransformer.init(w.model, w.weight_seed, snap_bf16=bf)
+    lat = P.build_lattice("grid2d", (w.L, w.L), periodic=True)
+    eng = P.LocalEnergyEngine(model, P.HamiltonianModel(lat), precision=precision)
+    port.set_bf16(bf)
+    om = port.model(w.model, w.weight_seed, snap_bf16=bf)
+    oh = port.hamiltonian("grid_periodic", w.L, w.L)
+    S = P.zero_sz_samples(w.n_sites, start, n_samples, w.sample_seed)
+    return w, eng, om, oh, S
+
+
+def run_parity(port, name, n_samples, start=0, taps_every=1, precision=None):
+    w, eng, om, oh, S = setup(port, name, n_samples, start, precision)
+    bf = eng.precision == "bf16"
+    ref_e, ref_im, ref_lpsi, ref_led = om.local_energies(oh, S, workers=os.cpu_count() or 8)
+    led = P.Ledger()
+    e, lpsi = eng.local_energies(S, led)
+    K, U, codes, lps = eng.taps(S)
+    # taps are a second GPU pass: they must reproduce the first bit for bit
+    if bf:
+        rep = ParityReport(window=BF16_WINDOW, logpsi_tol=BF16_LOGPSI_TOL,
+                           eloc_rtol=BF16_ELOC_RTOL)
+    else:
+        rep = ParityReport()
+    T = w.model.seq_len
+    for i in range(0, n_samples, taps_every):
+        taps = om.taps(oh, S[i])
+        assert taps.K == K[i]
+        compare(rep, taps, ref_e[i], ref_lpsi[i], codes[i], U[i], e[i].real, lpsi[i], lps[i], T)
+    print(f"\n[{name}] {rep.summary()}")
+    assert rep.ok(), rep.summary() + "\n" + "\n".join(rep.notes[:10])
+    if rep.clean_samples == rep.samples and taps_every == 1:
+        assert np.array_equal(led.as_array(), ref_led)
+    assert np.all(np.imag(e) == 0) and np.all(ref_im == 0)
+    return rep
+
+
+def test_c1_full_batch(port):
+    rep = run_parity(port, "c1", 256)
+    assert rep.clean_samples >= 0.95 * rep.samples
+
+
+def test_c2_parity(port):
+    rep = run_parity(port, "c2", 256)
+    assert rep.clean_samples >= 0.9 * rep.samples
+
+
+def test_c3_bf16_parity(port):
+    rep = run_parity(port, "c3", 24)
+    assert rep.clean_rows >= 0.8 * rep.rows
+    assert rep.logpsi_checked >= 0.5 * rep.samples
+
+
+def test_c3_fp32_strict(port):
+    rep = run_parity(port, "c3", 16, precision="fp32")
+    assert rep.clean_samples >= 0.5 * rep.samples
+
+
+def test_c4_bf16_parity_subset(port):
+    rep = run_parity(port, "c4", 2)
+    assert rep.clean_rows >= 0.5 * rep.rows
+
+
+@pytest.mark.slow
+def test_c4_fp32_strict_subset(port):
+    rep = run_parity(port, "c4", 2, precision="fp32")
+    assert rep.clean_rows >= 0.5 * rep.rows
+
+
+@pytest.mark.slow
+def test_c5_bf16_parity_subset(port):
+    rep = run_parity(port, "c5", 2)
+    assert rep.clean_rows >= 0.5 * rep.rows
+
+
+@pytest.mark.slow
+def test_c5_fp32_strict_subset(port):
+    rep = run_parity(port, "c5", 1, precision="fp32")
+    assert rep.clean_rows >= 0.5 * rep.rows
+
+
+def test_connected_log_probs_match_dedup_log_prob(port):
+    w, eng, om, oh, S = setup(port, "c1", 4)
+    for s in S:
+        lp = eng.connected_log_probs(s)
+        cf, _ = oh.connected_set(s)
+        ref = om.dedup_log_prob(cf, s)
+        assert lp.shape == ref.shape
+        np.testing.assert_allclose(lp, ref, atol=2e-5, rtol=0)
+
+
+def test_taps_reproduce_the_energy_pass(port):
+    w, eng, om, oh, S = setup(port, "c2", 16)
+    e, lpsi = eng.local_energies(S)
+    K, U, codes, lps = eng.taps(S)
+    for i in range(16):
+        assert 0.5 * lps[i][0] == lpsi[i]
+
+
+def test_chunking_and_batch_composition_invariance(port):
+    """Per-sample outputs do not depend on which other samples share a chunk
+    (no reduction mixes samples; SURVEY §7 hard part 8)."""
+    w, eng, om, oh, S = setup(port, "c2", 64)
+    e_all, l_all = eng.local_energies(S)
+    e_part, l_part = eng.local_energies(S[17:40])
+    assert np.array_equal(e_all[17:40], e_part)
+    assert np.array_equal(l_all[17:40], l_part)
+    e_rev, l_rev = eng.local_energies(S[::-1])
+    assert np.array_equal(e_all, e_rev[::-1])
+    assert np.array_equal(l_all, l_rev[::-1])
+
+
+def test_launch_count_reported(port):
+    w, eng, om, oh, S = setup(port, "c1", 8)
+    eng.local_energies(S)
+    assert eng.last_launch_count() > 10
