@@ -66,7 +66,7 @@ class ParityReport:
     def as_dict(self) -> dict:
         d = dict(self.__dict__)
         d.pop("notes")
-    return d
+        return d
 
     def summary(self) -> str:
         return (f"samples={self.samples} clean_samples={self.clean_samples} "
