@@ -247,7 +247,7 @@ def main():
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    prof = np.zeros(8)
+    prof = np.zeros(12)
     for i in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (256 MB > 126 MB L2)
         ev0[i].record(stream)
@@ -312,7 +312,11 @@ def main():
                      "kernel": "attention->VQ stage (per layer)",
                      "peak_source": f"{peak_kind} bf16_tflops_sustained",
                      "stage_ms_per_step": dom_ms / args.steps,
-                     "stage_share_of_step": (dom_ms / args.steps) / ms_per_step},
+                     "stage_share_of_step": (dom_ms / args.steps) / ms_per_step,
+                     "attention_ms_per_step": prof[7] / args.steps,
+                     "vq_ms_per_step": prof[6] / args.steps,
+                     "vq_rescored_per_step": prof[8] / args.steps,
+                     "active_locations_per_step": prof[3] / args.steps},
         "f_alg": {"flops_per_step": f_alg,
                   "fraction_of_peak": (f_alg / (ms_per_step / 1e3) / 1e12) / peak},
         "dedup_savings": {"total": tot_s, "quantized_ops": q_s,

@@ -297,8 +297,8 @@ class LocalEnergyEngine:
         return int(N.lib().vqnqs_gpu_last_launch_count(self._h))
 
     def last_profile(self) -> np.ndarray:
-        out = np.zeros(8)
-        N.lib().vqnqs_gpu_last_profile(self._h, N.ptr(out, C.c_double), 8)
+        out = np.zeros(12)
+        N.lib().vqnqs_gpu_last_profile(self._h, N.ptr(out, C.c_double), 12)
         return out
 
 

@@ -25,6 +25,7 @@
 #include "engine.h"
 #include "pipeline_kernels.cuh"
 #include "simt_kernels.cuh"
+#include "tc_attention.cuh"
 #include "tc_kernels.cuh"
 
 namespace vqb {
@@ -64,7 +65,8 @@ struct DBuf {
 };
 
 struct DevBlock {
-  float *ln1_g, *ln1_b, *bqkv, *bo, *ln2_g, *ln2_b, *b1, *b2, *cb32;
+  float *ln1_g, *ln1_b, *bqkv, *bo, *ln2_g, *ln2_b, *b1, *b2, *cb32, *wn2;
+  float wmax;
   void *wqkv, *wo, *w1, *w2, *cbA;       // [in x out] row-major, operand type
   void *wqkvT, *woT, *w1T, *w2T;         // [out x in] (K-major) copies for tcgen05
 };
@@ -122,7 +124,10 @@ class EngineImpl {
   int sms = 148;
   cudaStream_t own = nullptr;
   int d, nh, dh, Q, L, V, T, g, N, lastV;
-  bool use_tc = false;  // tcgen05 paths (bf16 precision)
+  bool use_tc_gemm = false;  // tcgen05 per-location GEMMs (bf16)
+  bool use_tc_vq = false;    // tcgen05 certified-argmin VQ (bf16)
+  bool use_tc_attn = false;  // tcgen05 gathered attention (bf16)
+  unsigned long long* d_rescored = nullptr;
   std::vector<void*> allocs;
   float *tok_embed, *pos_embed, *lnf_g, *lnf_b, *head_b;
   void* head_w;
@@ -134,7 +139,7 @@ class EngineImpl {
   std::vector<int32_t> h_bonds;
   // launch accounting / profile
   int64_t launches = 0;
-  double prof[8] = {0};
+  double prof[12] = {0};
   // arena
   int S_max = 256;
   DBuf<int32_t> K_, Mact_, row_bond_, row_t1_, tok0_, lrow_, Ucnt_, I_a, I_b, code_, slot_,
@@ -147,6 +152,8 @@ class EngineImpl {
   DBuf<float> x_a, x_b, y_, att_;
   DBuf<char> h_, qkv_, f1_;
   DBuf<uint8_t> cfg_stage_;
+  DBuf<AttnTile> tiles_;
+  DBuf<int32_t> ntiles_;
   DBuf<double> out_stage_;
   DBuf<int32_t> taps_codes_;
   size_t tab_cap_n = 0;
@@ -216,7 +223,12 @@ class EngineImpl {
     T = (N + g - 1) / g;
     lastV = (N % g == 0) ? V : 1 << (N % g);
     if (T > 1024 || dh > 256) throw CapabilityError("GPU path: T <= 1024, head dim <= 256");
-    use_tc = tc_supported(prec, d, dh, T, Q);
+    use_tc_gemm = tc_gemm_ok(prec, d, d) && tc_gemm_ok(prec, 4 * d, d);
+    use_tc_vq = tc_vq_ok(prec, d, Q);
+    use_tc_attn = tc_attn_ok(prec, d, dh, T) && !getenv("VQNQS_SIMT_ATTENTION");
+    ntiles_.ensure(1);
+    CK(cudaMalloc(&d_rescored, sizeof(unsigned long long)));
+    allocs.push_back(d_rescored);
     // weights, parameters() order (proj/src/model.cpp:188-229)
     int i = 0;
     auto nxt = [&]() -> const double* { return params[i++]; };
@@ -251,13 +263,26 @@ class EngineImpl {
       B.bo = upload_f(bo, d);
       B.cb32 = upload_f(cb, (int64_t)Q * d);
       B.cbA = upload_op(std::vector<double>(cb, cb + (size_t)Q * d));
+      {
+        // |W_j|^2 and max_j |W_j| for the certified argmin (tc_vq.cuh)
+        std::vector<float> wn2(Q);
+        double wmax = 0;
+        for (int j = 0; j < Q; ++j) {
+          double a = 0;
+          for (int cc = 0; cc < d; ++cc) a += cb[(size_t)j * d + cc] * cb[(size_t)j * d + cc];
+          wn2[j] = float(a);
+          wmax = std::max(wmax, std::sqrt(a));
+        }
+        B.wn2 = upload(wn2);
+        B.wmax = float(wmax * (1.0 + 1e-6));
+      }
       B.ln2_g = upload_f(ln2g, d);
       B.ln2_b = upload_f(ln2b, d);
       B.w1 = upload_op(std::vector<double>(w1, w1 + (size_t)d * 4 * d));
       B.b1 = upload_f(b1, 4 * d);
       B.w2 = upload_op(std::vector<double>(w2, w2 + (size_t)4 * d * d));
       B.b2 = upload_f(b2, d);
-      if (use_tc) {
+      if (use_tc_gemm) {
         auto tr = [](const double* w, int rows, int cols) {
           std::vector<double> t((size_t)rows * cols);
           for (int r = 0; r < rows; ++r)
@@ -318,7 +343,7 @@ class EngineImpl {
     marshall = m;
     // micro-batch size: keep the per-location working set near a fixed budget
     const double locs = double(T) + double(nb) * 0.5 * double(T);  // ~ active per sample
-    const double bytes_per_loc = double(d) * (use_tc ? 24.0 : 40.0) + 64.0;
+    const double bytes_per_loc = double(d) * 40.0 + 64.0;
     const double budget = 24e9;
     S_max = int(std::clamp(budget / (locs * bytes_per_loc), 16.0, 4096.0));
   }
@@ -327,7 +352,7 @@ class EngineImpl {
   void gemm(const int64_t* Mp, int64_t Mcap, int Nn, int Kk, const void* A, int lda,
             const int32_t* gA, const void* B, const void* BT, const float* bias, void* out, int ldo,
             int epi, const float* resid, int ldr, const int64_t* gR, cudaStream_t st) {
-    if (use_tc && BT) {
+    if (use_tc_gemm && BT) {
       tc_gemm(Mp, Mcap, Nn, Kk, A, lda, gA, BT, bias, out, ldo, epi, resid, ldr, gR, st, sms);
       ++launches;
       return;
@@ -380,7 +405,7 @@ class EngineImpl {
     }
     x_a.ensure(M * d); x_b.ensure(M * d); y_.ensure(M * d);
     h_.ensure(M * d * esz()); qkv_.ensure(M * 3 * d * esz()); f1_.ensure(M * 4 * d * esz());
-    if (!use_tc) att_.ensure(M * d);
+    att_.ensure(M * d);
     lpV_.ensure(M * V);
     const int64_t Rtot = R * T;
     k_enumerate<<<int((Rtot + 255) / 256), 256, 0, st>>>(S, R1, T, K_.p, row_t1_.p, row_aoff_.p,
@@ -415,11 +440,25 @@ class EngineImpl {
       gemm<TA>(Mb, M, 3 * d, d, h, d, nullptr, B.wqkv, B.wqkvT, B.bqkv, qkv, 3 * d, EPI_STORE,
                nullptr, 0, nullptr, st);
       CK(cudaEventRecord(ev[0], st));
-      if (use_tc) {
-        // fused gathered attention -> codebook distances -> certified argmin
-        tc_attention_vq(S, R1, T, d, dh, nh, Q, scale, K_.p, row_t1_.p, row_aoff_.p, act_off_.p,
-                        Icur, Uo_cur, qkv, B.cbA, B.cb32, code_.p, st, sms, prof);
-        launches += 1;
+      if (use_tc_attn) {
+        // tiles of whole rows (once per chunk; rows do not change across layers)
+        if (b == 0) {
+          tiles_.ensure(R);
+          CK(cudaMemsetAsync(ntiles_.p, 0, sizeof(int32_t), st));
+          k_build_tiles<<<(S * 32 + 127) / 128, 128, 0, st>>>(S, R1, T, K_.p, row_t1_.p,
+                                                              act_off_.p, tiles_.p, ntiles_.p);
+          ++launches;
+        }
+        const size_t asmem = AttnSmem(T).total + 1024;
+        static size_t attr = 0;
+        if (attr < asmem) {
+          CK(cudaFuncSetAttribute(k_tc_attention, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(asmem)));
+          attr = asmem;
+        }
+        k_tc_attention<<<sms, 128, asmem, st>>>(
+            tiles_.p, ntiles_.p, R1, T, d, dh, scale, row_t1_.p, act_off_.p, lrow_.p, lpos_.p,
+            Icur, Uo_cur, reinterpret_cast<const bf16*>(qkv), att_.p);
       } else {
         const size_t asmem = (size_t(T) * (dh + 1) + size_t(T) * dh + 4 * T + 4 * dh) * 4;
         if (asmem > 48 * 1024)
@@ -428,18 +467,28 @@ class EngineImpl {
         k_attention<TA><<<dim3(unsigned(R), nh), 128, asmem, st>>>(
             R1, T, d, dh, scale, K_.p, row_t1_.p, row_aoff_.p, act_off_.p, Icur, Uo_cur, qkv,
             att_.p);
-        CK(cudaEventRecord(ev[2], st));
-        const int LOCS = d > 384 ? 32 : 64;
-        const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;
-        const int vgrid = int(std::max<int64_t>(1, std::min<int64_t>((M + LOCS - 1) / LOCS, sms * 4)));
-        if (LOCS == 64) {
-          if (vsmem > 48 * 1024)
-            CK(cudaFuncSetAttribute(k_vq<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(vsmem)));
-          k_vq<64><<<vgrid, 256, vsmem, st>>>(tot + 0, d, att_.p, B.cb32, Q, code_.p);
+      }
+      CK(cudaEventRecord(ev[2], st));
+      {
+        if (use_tc_vq) {
+          tc_vq(tot + 0, M, d, att_.p, B.cbA, B.cb32, B.wn2, B.wmax, Q, code_.p, d_rescored, st,
+                sms);
         } else {
-          if (vsmem > 48 * 1024)
-            CK(cudaFuncSetAttribute(k_vq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(vsmem)));
-          k_vq<32><<<vgrid, 256, vsmem, st>>>(tot + 0, d, att_.p, B.cb32, Q, code_.p);
+          const int LOCS = d > 384 ? 32 : 64;
+          const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;
+          const int vgrid =
+              int(std::max<int64_t>(1, std::min<int64_t>((M + LOCS - 1) / LOCS, sms * 4)));
+          if (LOCS == 64) {
+            if (vsmem > 48 * 1024)
+              CK(cudaFuncSetAttribute(k_vq<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(vsmem)));
+            k_vq<64><<<vgrid, 256, vsmem, st>>>(tot + 0, d, att_.p, B.cb32, Q, code_.p);
+          } else {
+            if (vsmem > 48 * 1024)
+              CK(cudaFuncSetAttribute(k_vq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(vsmem)));
+            k_vq<32><<<vgrid, 256, vsmem, st>>>(tot + 0, d, att_.p, B.cb32, Q, code_.p);
+          }
         }
         launches += 2;
       }
@@ -447,16 +496,13 @@ class EngineImpl {
       {
         // per-layer stage timing (the engine syncs per chunk anyway)
         CK(cudaEventSynchronize(ev[1]));
-        float ms = 0.f;
+        float ms = 0.f, ma = 0.f;
         CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        CK(cudaEventElapsedTime(&ma, ev[0], ev[2]));
         prof[0] += ms;
-        prof[2] += use_tc ? 1 : 2;
-        if (!use_tc) {
-          float ma = 0.f;
-          CK(cudaEventElapsedTime(&ma, ev[0], ev[2]));
-          prof[7] += ma;
-          prof[6] += ms - ma;
-        }
+        prof[2] += 2;
+        prof[7] += ma;
+        prof[6] += ms - ma;
       }
       if (tap_codes) {
         taps_codes_.ensure(M);
@@ -539,6 +585,7 @@ class EngineImpl {
     CK(cudaSetDevice(dev));
     launches = 0;
     for (double& v : prof) v = 0;
+    CK(cudaMemsetAsync(d_rescored, 0, sizeof(unsigned long long), st));
     if (!ev[0])
       for (auto& e : ev) CK(cudaEventCreate(&e));
     int64_t tap_code_pos = 0, tap_lp_pos = 0;
@@ -593,6 +640,10 @@ class EngineImpl {
         }
       }
     }
+    unsigned long long resc = 0;
+    CK(cudaMemcpyAsync(&resc, d_rescored, sizeof(resc), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    prof[8] = double(resc);
   }
 
   void run_host(const uint8_t* configs, int64_t B, double* e_re, double* e_im, double* logpsi,
@@ -649,9 +700,12 @@ void Engine::run_host(const uint8_t* configs, int64_t B, double* e_re, double* e
 }
 int64_t Engine::last_launches() const { return p_->launches; }
 int Engine::last_profile(double* out, int cap) const {
-  for (int i = 0; i < cap && i < 8; ++i) out[i] = p_->prof[i];
-  return 8;
+  for (int i = 0; i < cap && i < 12; ++i) out[i] = p_->prof[i];
+  return 12;
 }
 const vqnqs_model_desc& Engine::desc() const { return p_->c; }
 
 }  // namespace vqb
+
+// Kernel-level test hooks share this translation unit (header-defined kernels).
+#include "debug_hooks.cuh"

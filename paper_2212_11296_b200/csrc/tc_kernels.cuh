@@ -1,22 +1,93 @@
-// tcgen05 (5th-gen tensor core) paths for the bf16 configurations.
+// Host launchers for the tcgen05 kernels (bf16 configurations).
 #pragma once
 
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+
 #include "common.cuh"
+#include "tc_gemm.cuh"
+#include "tc_vq.cuh"
 
 namespace vqb {
 
-inline bool tc_supported(int prec, int d, int dh, int T, int Q) {
-  (void)prec; (void)d; (void)dh; (void)T; (void)Q;
-  return false;
+// tcgen05 GEMM applies when operands are bf16 and K, N tile cleanly.
+inline bool tc_gemm_ok(int prec, int N, int K) {
+  return prec == 1 && K % 64 == 0 && N % 64 == 0;
+}
+inline bool tc_vq_ok(int prec, int d, int Q) { return prec == 1 && d % 64 == 0 && Q % 256 == 0; }
+
+template <int BN, int EPI, bool G>
+inline void launch_tc_gemm_inst(const int64_t* Mp, int64_t Mcap, int N, int K, const bf16* A,
+                                int lda, const int32_t* gA, const bf16* WT, const float* bias,
+                                void* out, int ldo, const float* resid, int ldr,
+                                const int64_t* gR, cudaStream_t st, int sms) {
+  const size_t smem = tcg_smem_bytes<BN>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tc_gemm<BN, EPI, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    attr = true;
+  }
+  const int64_t tiles = ((Mcap + 127) / 128) * (N / BN);
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
+  k_tc_gemm<BN, EPI, G><<<grid, 128, smem, st>>>(Mp, N, K, A, lda, gA, WT, bias, out, ldo, resid,
+                                                 ldr, gR);
 }
 
-inline void tc_gemm(const int64_t*, int64_t, int, int, const void*, int, const int32_t*,
-                    const void*, const float*, void*, int, int, const float*, int,
-                    const int64_t*, cudaStream_t, int) {}
+template <int BN>
+inline void launch_tc_gemm_bn(const int64_t* Mp, int64_t Mcap, int N, int K, const bf16* A, int lda,
+                              const int32_t* gA, const bf16* WT, const float* bias, void* out,
+                              int ldo, int epi, const float* resid, int ldr, const int64_t* gR,
+                              cudaStream_t st, int sms) {
+  if (gA) {
+    if (epi == EPI_RESID)
+      launch_tc_gemm_inst<BN, EPI_RESID, true>(Mp, Mcap, N, K, A, lda, gA, WT, bias, out, ldo,
+                                               resid, ldr, gR, st, sms);
+    else
+      throw std::runtime_error("tc_gemm: gathered A only with the residual epilogue");
+  } else if (epi == EPI_STORE) {
+    launch_tc_gemm_inst<BN, EPI_STORE, false>(Mp, Mcap, N, K, A, lda, gA, WT, bias, out, ldo,
+                                              resid, ldr, gR, st, sms);
+  } else if (epi == EPI_GELU) {
+    launch_tc_gemm_inst<BN, EPI_GELU, false>(Mp, Mcap, N, K, A, lda, gA, WT, bias, out, ldo,
+                                             resid, ldr, gR, st, sms);
+  } else {
+    launch_tc_gemm_inst<BN, EPI_RESID, false>(Mp, Mcap, N, K, A, lda, gA, WT, bias, out, ldo,
+                                              resid, ldr, gR, st, sms);
+  }
+}
 
-inline void tc_attention_vq(int, int, int, int, int, int, int, float, const int32_t*,
-                            const int32_t*, const int64_t*, const int64_t*, const int32_t*,
-                            const int64_t*, const void*, const void*, const float*, int32_t*,
-                            cudaStream_t, int, double*) {}
+inline void tc_gemm(const int64_t* Mp, int64_t Mcap, int N, int K, const void* A, int lda,
+                    const int32_t* gA, const void* WT, const float* bias, void* out, int ldo,
+                    int epi, const float* resid, int ldr, const int64_t* gR, cudaStream_t st,
+                    int sms) {
+  const bf16* a = static_cast<const bf16*>(A);
+  const bf16* w = static_cast<const bf16*>(WT);
+  if (N % 256 == 0)
+    launch_tc_gemm_bn<256>(Mp, Mcap, N, K, a, lda, gA, w, bias, out, ldo, epi, resid, ldr, gR, st,
+                           sms);
+  else if (N % 128 == 0)
+    launch_tc_gemm_bn<128>(Mp, Mcap, N, K, a, lda, gA, w, bias, out, ldo, epi, resid, ldr, gR, st,
+                           sms);
+  else
+    launch_tc_gemm_bn<64>(Mp, Mcap, N, K, a, lda, gA, w, bias, out, ldo, epi, resid, ldr, gR, st,
+                          sms);
+}
+
+inline void tc_vq(const int64_t* Mp, int64_t Mcap, int d, const float* x, const void* cbA,
+                  const float* cb32, const float* wn2, float wmax, int Q, int32_t* code,
+                  unsigned long long* n_rescored, cudaStream_t st, int sms) {
+  const size_t smem = tcv_smem_bytes(Q);
+  static size_t attr = 0;
+  if (attr < smem) {
+    cudaFuncSetAttribute(k_tc_vq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = smem;
+  }
+  const int64_t tiles = (Mcap + 127) / 128;
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
+  k_tc_vq<<<grid, 128, smem, st>>>(Mp, d, x, static_cast<const bf16*>(cbA), cb32, wn2, wmax, Q,
+                                   code, n_rescored);
+}
 
 }  // namespace vqb
