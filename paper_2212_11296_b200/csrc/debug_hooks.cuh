@@ -71,7 +71,20 @@ extern "C" int vqnqs_debug_vq(int64_t M, int d, const float* x, const float* cb3
   cudaMemcpy(dwn2, wn2.data(), Q * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dcb, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice);
   if (use_tc) {
-    tc_vq(dM, M, d, x, dcb, cb32, dwn2, float(wmax * (1 + 1e-6)), Q, code, n_rescored, 0, sms);
+    bf16 *xh = nullptr, *xl = nullptr;
+    float *xn2 = nullptr, *rr2 = nullptr;
+    cudaMalloc(&xh, size_t(M) * d * 2);
+    cudaMalloc(&xl, size_t(M) * d * 2);
+    cudaMalloc(&xn2, size_t(M) * 4);
+    cudaMalloc(&rr2, size_t(M) * 4);
+    k_vq_prep<<<sms * 4, 256>>>(dM, d, x, xh, xl, xn2, rr2);
+    tc_vq(dM, M, d, xh, xl, xn2, rr2, dcb, cb32, dwn2, float(wmax * (1 + 1e-6)), Q, code,
+          n_rescored, 0, sms);
+    cudaDeviceSynchronize();
+    cudaFree(xh);
+    cudaFree(xl);
+    cudaFree(xn2);
+    cudaFree(rr2);
   } else {
     const int LOCS = d > 384 ? 32 : 64;
     const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;

@@ -149,7 +149,8 @@ class EngineImpl {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   DBuf<double> diag_, lpV_, lp_rows_;
   DBuf<unsigned long long> tkey_;
-  DBuf<float> x_a, x_b, y_, att_;
+  DBuf<float> x_a, x_b, y_, att_, xn2_, rr2_;
+  DBuf<bf16> att_hi_, att_lo_;
   DBuf<char> h_, qkv_, f1_;
   DBuf<uint8_t> cfg_stage_;
   DBuf<AttnTile> tiles_;
@@ -321,7 +322,7 @@ class EngineImpl {
     lpos_.release(); upos_.release(); row_aoff_.release(); act_off_.release(); tab_off_.release();
     Uoff_.release(); tot_.release(); g_res_.release(); attw_.release(); diag_.release(); lpV_.release();
     lp_rows_.release(); tkey_.release(); x_a.release(); x_b.release(); y_.release();
-    att_.release(); h_.release(); qkv_.release(); f1_.release(); cfg_stage_.release();
+    att_.release(); xn2_.release(); rr2_.release(); att_hi_.release(); att_lo_.release(); h_.release(); qkv_.release(); f1_.release(); cfg_stage_.release();
     out_stage_.release(); taps_codes_.release();
   }
 
@@ -405,7 +406,13 @@ class EngineImpl {
     }
     x_a.ensure(M * d); x_b.ensure(M * d); y_.ensure(M * d);
     h_.ensure(M * d * esz()); qkv_.ensure(M * 3 * d * esz()); f1_.ensure(M * 4 * d * esz());
-    att_.ensure(M * d);
+    if (!use_tc_attn) att_.ensure(M * d);  // fp32 attention rows (CUDA-core path)
+    if (use_tc_vq) {
+      att_hi_.ensure(M * d);
+      att_lo_.ensure(M * d);
+      xn2_.ensure(M);
+      rr2_.ensure(M);
+    }
     lpV_.ensure(M * V);
     const int64_t Rtot = R * T;
     k_enumerate<<<int((Rtot + 255) / 256), 256, 0, st>>>(S, R1, T, K_.p, row_t1_.p, row_aoff_.p,
@@ -456,9 +463,9 @@ class EngineImpl {
                                   int(asmem)));
           attr = asmem;
         }
-        k_tc_attention<<<sms, 128, asmem, st>>>(
+        k_tc_attention<<<sms, TCA_THREADS, asmem, st>>>(
             tiles_.p, ntiles_.p, R1, T, d, dh, scale, row_t1_.p, act_off_.p, lrow_.p, lpos_.p,
-            Icur, Uo_cur, reinterpret_cast<const bf16*>(qkv), att_.p);
+            Icur, Uo_cur, reinterpret_cast<const bf16*>(qkv), att_hi_.p, att_lo_.p, xn2_.p, rr2_.p);
       } else {
         const size_t asmem = (size_t(T) * (dh + 1) + size_t(T) * dh + 4 * T + 4 * dh) * 4;
         if (asmem > 48 * 1024)
@@ -471,8 +478,13 @@ class EngineImpl {
       CK(cudaEventRecord(ev[2], st));
       {
         if (use_tc_vq) {
-          tc_vq(tot + 0, M, d, att_.p, B.cbA, B.cb32, B.wn2, B.wmax, Q, code_.p, d_rescored, st,
-                sms);
+          if (!use_tc_attn) {
+            k_vq_prep<<<sms * 8, 256, 0, st>>>(tot + 0, d, att_.p, att_hi_.p, att_lo_.p, xn2_.p,
+                                               rr2_.p);
+            ++launches;
+          }
+          tc_vq(tot + 0, M, d, att_hi_.p, att_lo_.p, xn2_.p, rr2_.p, B.cbA, B.cb32, B.wn2, B.wmax, Q,
+                code_.p, d_rescored, st, sms);
         } else {
           const int LOCS = d > 384 ? 32 : 64;
           const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;

@@ -7,10 +7,10 @@
 // query at (row k, position p >= a_k) the keys are the base row's at
 // positions t < a_k and row k's own active locations a_k <= t <= p. The own
 // keys of every row in the tile are the tile's own locations, so per head:
-//   S_base = Q K_base^T   (M=128, N=T_pad)   base row's keys
-//   S_own  = Q K_tile^T   (M=128, N=128)     the tile's own keys
+//   S_base = Q K_base^T   (M=128, N=16*ceil(max a/16))   base row's keys
+//   S_own  = Q K_tile^T   (M=128, N=128)                 the tile's own keys
 //   softmax per query over S_base[:, :a_k] and S_own[:, seg_k .. i]
-//   O      = P_base V_base + P_own V_tile    (M=128, N=dh)
+//   O      = P_base V_base + P_own V_tile                (M=128, N=dh)
 // Scores are scaled after the product and the normalised probabilities are
 // rounded to bf16 before the value product, exactly where the reference's
 // product boundary rounds under bf16 emulation.
@@ -18,9 +18,16 @@
 // All operands are staged with cp.async per 64-wide head group as SW128
 // tiles [rows x 64]: Q/K are K-major operands; V, staged the same way
 // (key rows, 64 head-dims contiguous), is the MN-major B operand of the value
-// product, so nothing is transposed. The softmax reads only the warp's live
-// score columns, in two TMEM passes (online max/sum, then probabilities).
+// product, so nothing is transposed. Softmax: three TMEM passes over only
+// the warp's live columns (max; exp2 + sum, exponentials stored back to
+// TMEM; normalise + bf16 into the P tiles) so each score costs one MUFU op.
 // TMEM: S_base | S_own | O(group) = T_pad + 128 + 64 <= 512 columns.
+//
+// Outputs per active location: the attention row x as its two-term bf16
+// split xh = bf16(x), xl = bf16(x - xh) (the VQ distance GEMM operands; x is
+// represented to 2^-18 relative), |x|^2 and |x - xh - xl|^2 (the certified
+// argmin error bound, tc_vq.cuh). 512 threads: warp w owns TMEM lanes
+// 32(w%4).. (its query rows); the four warpgroups split the score columns.
 #pragma once
 
 #include "common.cuh"
@@ -67,7 +74,7 @@ __host__ __device__ inline int attn_kb_base(int T) { return (attn_tpad(T) + 63) 
 
 // shared memory carve (bytes, all sub-tiles 1024-aligned)
 struct AttnSmem {
-  uint32_t q, kown, vown, kbase, vbase, pbase, pown, bar, total;
+  uint32_t q, kown, vown, kbase, vbase, pbase, pown, rows, bar, total;
   __host__ __device__ AttnSmem(int T) {
     const uint32_t KBb = (uint32_t)attn_kb_base(T);
     q = 0;                             // 128 x 64
@@ -77,7 +84,8 @@ struct AttnSmem {
     vbase = kbase + 64 * KBb * 128;    // (64*KBb) x 64
     pbase = vbase + 64 * KBb * 128;    // P base: 128 x (64*KBb) in KBb blocks
     pown = pbase + KBb * 128 * 128;    // P own: 128 x 128 in 2 blocks
-    bar = pown + 2 * 128 * 128;
+    rows = pown + 2 * 128 * 128;       // int64 row offsets: 128 tile + 128 base
+    bar = rows + 256 * 8;
     total = bar + 64;
   }
 };
@@ -85,23 +93,31 @@ struct AttnSmem {
 __device__ __forceinline__ int warp_max_i(int v) { return __reduce_max_sync(0xffffffffu, v); }
 __device__ __forceinline__ int warp_min_i(int v) { return __reduce_min_sync(0xffffffffu, v); }
 
-__global__ void __launch_bounds__(128, 1) k_tc_attention(
+constexpr int TCA_THREADS = 512;
+
+__global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     const AttnTile* __restrict__ tiles, const int32_t* __restrict__ n_tiles_p, int R1, int T,
     int d, int dh, float scale, const int32_t* __restrict__ row_t1,
     const int64_t* __restrict__ act_off, const int32_t* __restrict__ lrow,
     const int16_t* __restrict__ lpos, const int32_t* __restrict__ I,
-    const int64_t* __restrict__ Uoff, const bf16* __restrict__ qkv, float* __restrict__ att) {
+    const int64_t* __restrict__ Uoff, const bf16* __restrict__ qkv, bf16* __restrict__ xh_out,
+    bf16* __restrict__ xl_out, float* __restrict__ xn2_out, float* __restrict__ rr2_out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const AttnSmem L(T);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+  int64_t* rowq = reinterpret_cast<int64_t*>(smem + L.rows);  // qkv offsets of tile rows
+  int64_t* rowb = rowq + 128;                                 // ... of base rows
+  __shared__ float red[4][128];
+  __shared__ float red2[4][128];
   __shared__ int s_amax;
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int TP = attn_tpad(T);
+  const int row = tid & 127, part = tid >> 7;  // warp w drains TMEM lanes 32(w%4)..
   const int KBb = attn_kb_base(T);
   const int n_tiles = *n_tiles_p;
+  const int TP = attn_tpad(T);
   if (tid == 0) {
     tc::mbar_init(&mbar[0], 1);
     tc::mbar_init(&mbar[1], 1);
@@ -114,7 +130,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_attention(
   const uint32_t tmem = *tmem_slot;
   const uint32_t sb = tc::smem_u32(smem);
   const uint32_t TS_BASE = 0, TS_OWN = (uint32_t)TP, TS_O = (uint32_t)TP + 128;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const int ld = 3 * d;
   const int G = d / 64;
   const int hpg = 64 / dh;  // heads per 64-wide group
@@ -126,45 +142,48 @@ __global__ void __launch_bounds__(128, 1) k_tc_attention(
     const int s = tile.sample;
     const int64_t uo = Uoff[s];
     const int64_t base = act_off[s];
-    // this thread's query (tile row tid): base keys [0, a), own keys [own_lo, tid]
-    const bool live = tid < tile.nloc;
-    int a = 0, own_lo = tid + 1, own_hi = tid;
+    // this thread's query (tile row `row`): base keys [0, a), own keys [own_lo, own_hi]
+    const bool live = row < tile.nloc;
+    int a = 0, own_lo = 1 << 20, own_hi = -1;
     int64_t myloc = 0;
+    if (tid == 0) s_amax = 0;
+    if (part == 0) {
+      rowq[row] = live ? (uo + I[tile.loc0 + row]) * ld : -1;
+      rowb[row] = row < T ? (uo + I[base + row]) * ld : -1;
+    }
     if (live) {
-      myloc = tile.loc0 + tid;
+      myloc = tile.loc0 + row;
       const int r = lrow[myloc];
       const int p = lpos[myloc];
       a = (r % R1) == 0 ? 0 : row_t1[r] + 1;
-      own_lo = tid - (p - a);
-    } else {
-      own_lo = 1 << 20;
-      own_hi = -1;
+      own_lo = row - (p - a);
+      own_hi = row;
     }
-    if (tid == 0) s_amax = 0;
     __syncthreads();
-    atomicMax(&s_amax, a);
-    // warp-uniform live column ranges
-    const int w_amax = warp_max_i(a);
+    if (part == 0) atomicMax(&s_amax, a);
+    // warp-uniform live column ranges (16-column chunks)
+    const int wb_end = (warp_max_i(a) + 15) & ~15;
     const int w_olo = warp_min_i(own_lo), w_ohi = warp_max_i(own_hi);
-    const int wb_end = (w_amax + 15) & ~15;
-    const int wo_beg = w_olo >= 128 ? 128 : (w_olo & ~15), wo_end = (w_ohi + 16) & ~15;
+    const int wo_beg = w_olo >= 128 ? 128 : (w_olo & ~15);
+    const int wo_end = w_ohi < 0 ? 0 : ((w_ohi + 16) & ~15);
+    float xn2 = 0.f, rr2 = 0.f;
     for (int gi = 0; gi < G; ++gi) {
       // ---- stage the group's operands (cp.async, zero-filled tails)
-      for (int e = tid; e < 128 * 8; e += 128) {
+      for (int e = tid; e < 128 * 8; e += TCA_THREADS) {
         const int r = e >> 3, c = e & 7;
-        const bool ok = r < tile.nloc;
-        const int64_t u = ok ? uo + I[tile.loc0 + r] : 0;
-        const bf16* src = qkv + u * ld + gi * 64 + c * 8;
+        const int64_t off = rowq[r];
+        const bool ok = off >= 0;
+        const bf16* src = qkv + (ok ? off : 0) + gi * 64 + c * 8;
         const uint32_t o = tc::sw128_chunk(r, c);
         tc::cp_async16_zfill(sb + L.q + o, src, ok);
         tc::cp_async16_zfill(sb + L.kown + o, src + d, ok);
         tc::cp_async16_zfill(sb + L.vown + o, src + 2 * d, ok);
       }
-      for (int e = tid; e < 64 * KBb * 8; e += 128) {
+      for (int e = tid; e < 64 * KBb * 8; e += TCA_THREADS) {
         const int t = e >> 3, c = e & 7;
-        const bool ok = t < T;
-        const int64_t u = ok ? uo + I[base + t] : 0;
-        const bf16* src = qkv + u * ld + d + gi * 64 + c * 8;
+        const int64_t off = t < 128 ? rowb[t] : -1;
+        const bool ok = off >= 0;
+        const bf16* src = qkv + (ok ? off : 0) + d + gi * 64 + c * 8;
         const uint32_t o = tc::sw128_chunk(t, c);
         tc::cp_async16_zfill(sb + L.kbase + o, src, ok);
         tc::cp_async16_zfill(sb + L.vbase + o, src + d, ok);
@@ -173,8 +192,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_attention(
       tc::cp_async_wait<0>();
       tc::fence_proxy_async();
       __syncthreads();
-      const int t_amax = s_amax;
-      const int kb_base = (t_amax + 15) & ~15;  // base keys any row uses
+      const int kb_base = (s_amax + 15) & ~15;  // base keys any row of the tile uses
       for (int hh = 0; hh < hpg; ++hh) {
         const uint32_t koff = (uint32_t)(hh * dh * 2);  // head offset inside the 128-B row
         // ---- scores
@@ -194,79 +212,85 @@ __global__ void __launch_bounds__(128, 1) k_tc_attention(
         tc::mbar_wait(&mbar[0], ph_s);
         ph_s ^= 1;
         tc::fence_after();
-        // ---- pass 1: online max / sum over the live columns (log2 domain)
-        float m = -INFINITY, sum = 0.f;
-        for (int c0 = 0; c0 < wb_end; c0 += 16) {
+        // ---- pass 1: row max; warpgroup `part` owns 16-column chunks part, part+4, ...
+        float m = -INFINITY;
+        for (int c0 = part * 16; c0 < wb_end; c0 += 64) {
           float v[16];
           tc::tmem_ld16(trow + TS_BASE + c0, v);
           tc::tmem_wait_ld();
-          float cm = -INFINITY;
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (c0 + j < a) cm = fmaxf(cm, v[j] * sl2);
-          if (cm > m) {
-            sum *= exp2f(m - cm);
-            m = cm;
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < a) sum += exp2f(v[j] * sl2 - m);
+            if (c0 + j < a) m = fmaxf(m, v[j]);
         }
-        for (int c0 = wo_beg; c0 < wo_end; c0 += 16) {
+        for (int c0 = wo_beg + part * 16; c0 < wo_end; c0 += 64) {
           float v[16];
           tc::tmem_ld16(trow + TS_OWN + c0, v);
           tc::tmem_wait_ld();
-          float cm = -INFINITY;
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (c0 + j >= own_lo && c0 + j <= own_hi) cm = fmaxf(cm, v[j] * sl2);
-          if (cm > m) {
-            sum *= exp2f(m - cm);
-            m = cm;
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j >= own_lo && c0 + j <= own_hi) sum += exp2f(v[j] * sl2 - m);
+            if (c0 + j >= own_lo && c0 + j <= own_hi) m = fmaxf(m, v[j]);
         }
-        const float inv = 1.f / sum;
-        // ---- pass 2: bf16 probabilities into the P tiles (zeros elsewhere)
-        for (int c0 = 0; c0 < kb_base; c0 += 16) {
+        red[part][row] = m;
+        __syncthreads();
+        m = fmaxf(fmaxf(red[0][row], red[1][row]), fmaxf(red[2][row], red[3][row])) * sl2;
+        // ---- pass 2: e = exp2(s*scale*log2e - m) on live entries (0 elsewhere), back to TMEM
+        float sum = 0.f;
+        for (int c0 = part * 16; c0 < wb_end; c0 += 64) {
           float v[16];
+          tc::tmem_ld16(trow + TS_BASE + c0, v);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            v[j] = (c0 + j < a) ? exp2f(fmaf(v[j], sl2, -m)) : 0.f;
+            sum += v[j];
+          }
+          tc::tmem_st16(trow + TS_BASE + c0, v);
+        }
+        for (int c0 = wo_beg + part * 16; c0 < wo_end; c0 += 64) {
+          float v[16];
+          tc::tmem_ld16(trow + TS_OWN + c0, v);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            v[j] = (c0 + j >= own_lo && c0 + j <= own_hi) ? exp2f(fmaf(v[j], sl2, -m)) : 0.f;
+            sum += v[j];
+          }
+          tc::tmem_st16(trow + TS_OWN + c0, v);
+        }
+        tc::tmem_wait_st();
+        red2[part][row] = sum;
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        const float inv = 1.f / (((red2[0][row] + red2[1][row]) + red2[2][row]) + red2[3][row]);
+        // ---- pass 3: normalised bf16 probabilities into the P tiles
+        for (int c0 = part * 16; c0 < kb_base; c0 += 64) {
+          uint32_t pk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
           if (c0 < wb_end) {
+            float v[16];
             tc::tmem_ld16(trow + TS_BASE + c0, v);
             tc::tmem_wait_ld();
-          }
-          uint32_t pk[8];
 #pragma unroll
-          for (int j = 0; j < 16; j += 2) {
-            const float p0 = (c0 + j < a) ? exp2f(v[j] * sl2 - m) * inv : 0.f;
-            const float p1 = (c0 + j + 1 < a) ? exp2f(v[j + 1] * sl2 - m) * inv : 0.f;
-            pk[j / 2] = tc::pack_bf16(p0, p1);
+            for (int j = 0; j < 16; j += 2) pk[j / 2] = tc::pack_bf16(v[j] * inv, v[j + 1] * inv);
           }
           const uint32_t blk = sb + L.pbase + (uint32_t)(c0 >> 6) * (128 * 128);
           const uint32_t cc = (uint32_t)((c0 & 63) >> 3);
-          tc::st_shared_v4(blk + tc::sw128_chunk(tid, cc), pk[0], pk[1], pk[2], pk[3]);
-          tc::st_shared_v4(blk + tc::sw128_chunk(tid, cc + 1), pk[4], pk[5], pk[6], pk[7]);
+          tc::st_shared_v4(blk + tc::sw128_chunk(row, cc), pk[0], pk[1], pk[2], pk[3]);
+          tc::st_shared_v4(blk + tc::sw128_chunk(row, cc + 1), pk[4], pk[5], pk[6], pk[7]);
         }
-        for (int c0 = 0; c0 < 128; c0 += 16) {
-          float v[16];
-          const bool in = c0 >= wo_beg && c0 < wo_end;
-          if (in) {
+        for (int c0 = part * 16; c0 < 128; c0 += 64) {
+          uint32_t pk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          if (c0 >= wo_beg && c0 < wo_end) {
+            float v[16];
             tc::tmem_ld16(trow + TS_OWN + c0, v);
             tc::tmem_wait_ld();
-          }
-          uint32_t pk[8];
 #pragma unroll
-          for (int j = 0; j < 16; j += 2) {
-            const int t0 = c0 + j, t1 = c0 + j + 1;
-            const float p0 = (in && t0 >= own_lo && t0 <= own_hi) ? exp2f(v[j] * sl2 - m) * inv : 0.f;
-            const float p1 = (in && t1 >= own_lo && t1 <= own_hi) ? exp2f(v[j + 1] * sl2 - m) * inv : 0.f;
-            pk[j / 2] = tc::pack_bf16(p0, p1);
+            for (int j = 0; j < 16; j += 2) pk[j / 2] = tc::pack_bf16(v[j] * inv, v[j + 1] * inv);
           }
           const uint32_t blk = sb + L.pown + (uint32_t)(c0 >> 6) * (128 * 128);
           const uint32_t cc = (uint32_t)((c0 & 63) >> 3);
-          tc::st_shared_v4(blk + tc::sw128_chunk(tid, cc), pk[0], pk[1], pk[2], pk[3]);
-          tc::st_shared_v4(blk + tc::sw128_chunk(tid, cc + 1), pk[4], pk[5], pk[6], pk[7]);
+          tc::st_shared_v4(blk + tc::sw128_chunk(row, cc), pk[0], pk[1], pk[2], pk[3]);
+          tc::st_shared_v4(blk + tc::sw128_chunk(row, cc + 1), pk[4], pk[5], pk[6], pk[7]);
         }
         tc::fence_before();
         tc::fence_proxy_async();
@@ -300,22 +324,44 @@ __global__ void __launch_bounds__(128, 1) k_tc_attention(
         ph_o ^= 1;
         tc::fence_after();
       }
-      // ---- drain the group's O (64 cols) to the fp32 attention output
-      for (int c0 = 0; c0 < 64; c0 += 16) {
+      // ---- drain the group's O: warpgroup `part` takes columns [16 part, 16 part + 16)
+      {
         float v[16];
-        tc::tmem_ld16(trow + TS_O + c0, v);
+        tc::tmem_ld16(trow + TS_O + part * 16, v);  // warp-collective: every lane loads
         tc::tmem_wait_ld();
         if (live) {
-          float4* o = reinterpret_cast<float4*>(att + myloc * d + gi * 64 + c0);
-          o[0] = make_float4(v[0], v[1], v[2], v[3]);
-          o[1] = make_float4(v[4], v[5], v[6], v[7]);
-          o[2] = make_float4(v[8], v[9], v[10], v[11]);
-          o[3] = make_float4(v[12], v[13], v[14], v[15]);
+          uint32_t ph[8], pl[8];
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {
+            ph[j / 2] = tc::pack_bf16(v[j], v[j + 1]);
+            const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&ph[j / 2]);
+            const float d0 = v[j] - __low2float(h), d1 = v[j + 1] - __high2float(h);
+            pl[j / 2] = tc::pack_bf16(d0, d1);
+            const __nv_bfloat162 l = *reinterpret_cast<const __nv_bfloat162*>(&pl[j / 2]);
+            const float r0 = d0 - __low2float(l), r1 = d1 - __high2float(l);
+            xn2 = fmaf(v[j], v[j], fmaf(v[j + 1], v[j + 1], xn2));
+            rr2 = fmaf(r0, r0, fmaf(r1, r1, rr2));
+          }
+          uint4* oh = reinterpret_cast<uint4*>(xh_out + myloc * d + gi * 64 + part * 16);
+          uint4* ol = reinterpret_cast<uint4*>(xl_out + myloc * d + gi * 64 + part * 16);
+          oh[0] = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+          oh[1] = make_uint4(ph[4], ph[5], ph[6], ph[7]);
+          ol[0] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+          ol[1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
         }
       }
       tc::fence_before();
       __syncthreads();
     }
+    // row norms: |x|^2 and |x - xh - xl|^2, reduced over the four warpgroups
+    red[part][row] = xn2;
+    red2[part][row] = rr2;
+    __syncthreads();
+    if (part == 0 && live) {
+      xn2_out[myloc] = ((red[0][row] + red[1][row]) + red[2][row]) + red[3][row];
+      rr2_out[myloc] = ((red2[0][row] + red2[1][row]) + red2[2][row]) + red2[3][row];
+    }
+    __syncthreads();
   }
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem, 512);

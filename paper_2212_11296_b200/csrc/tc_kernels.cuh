@@ -75,8 +75,40 @@ inline void tc_gemm(const int64_t* Mp, int64_t Mcap, int N, int K, const void* A
                           sms);
 }
 
-inline void tc_vq(const int64_t* Mp, int64_t Mcap, int d, const float* x, const void* cbA,
-                  const float* cb32, const float* wn2, float wmax, int Q, int32_t* code,
+// bf16 copy and |x|^2, |x - bf16(x)|^2 of fp32 attention rows, for the VQ
+// operand when the attention ran on CUDA cores (the tcgen05 attention
+// epilogue writes these itself). One warp per row.
+__global__ void k_vq_prep(const int64_t* __restrict__ Mp, int d, const float* __restrict__ x,
+                          bf16* __restrict__ xh, bf16* __restrict__ xl, float* __restrict__ xn2,
+                          float* __restrict__ rr2) {
+  const int64_t M = *Mp;
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
+    float n2 = 0.f, q2 = 0.f;
+    for (int c = lane; c < d; c += 32) {
+      const float v = x[r * d + c];
+      const bf16 h = __float2bfloat16_rn(v);
+      const float df = v - __bfloat162float(h);
+      const bf16 l = __float2bfloat16_rn(df);
+      const float rr = df - __bfloat162float(l);
+      xh[r * d + c] = h;
+      xl[r * d + c] = l;
+      n2 = fmaf(v, v, n2);
+      q2 = fmaf(rr, rr, q2);
+    }
+    n2 = warp_sum(n2);
+    q2 = warp_sum(q2);
+    if (lane == 0) {
+      xn2[r] = n2;
+      rr2[r] = q2;
+    }
+  }
+}
+
+inline void tc_vq(const int64_t* Mp, int64_t Mcap, int d, const bf16* xh, const bf16* xl,
+                  const float* xn2, const float* rr2, const void* cbA, const float* cb32,
+                  const float* wn2, float wmax, int Q, int32_t* code,
                   unsigned long long* n_rescored, cudaStream_t st, int sms) {
   const size_t smem = tcv_smem_bytes(Q);
   static size_t attr = 0;
@@ -86,8 +118,8 @@ inline void tc_vq(const int64_t* Mp, int64_t Mcap, int d, const float* x, const 
   }
   const int64_t tiles = (Mcap + 127) / 128;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
-  k_tc_vq<<<grid, 128, smem, st>>>(Mp, d, x, static_cast<const bf16*>(cbA), cb32, wn2, wmax, Q,
-                                   code, n_rescored);
+  k_tc_vq<<<grid, TCV_THREADS, smem, st>>>(Mp, d, xh, xl, xn2, rr2, static_cast<const bf16*>(cbA),
+                                           cb32, wn2, wmax, Q, code, n_rescored);
 }
 
 }  // namespace vqb
