@@ -217,20 +217,14 @@ def main():
     stream = torch.cuda.current_stream()
     flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=f"cuda:{local}")
 
-    def stats_allreduce(e):
-        # fill_stats (proj/src/trainer.cpp:184-198) across ranks: one fp64
-        # allreduce of {n, sum E, sum E^2, sum Im E} (NCCL over NVLink)
-        v = torch.stack([torch.tensor(float(B), dtype=torch.float64, device=e.device),
-                         e.sum(), (e * e).sum(), torch.zeros((), dtype=torch.float64,
-                                                              device=e.device)])
-        if ws > 1:
-            dist.all_reduce(v)
-        return v
+    from paper_2212_11296_b200.distributed import allreduce_stats
 
     def step():
         led = eng.local_energies_device(d_cfg, d_e, d_l, stream)
-        v = stats_allreduce(d_e)
-        return led, v
+        # fill_stats (proj/src/trainer.cpp:184-198) over all ranks: the only
+        # collective (two small fp64 allreduces, NCCL over NVLink)
+        est = allreduce_stats(d_e)
+        return led, est
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -275,11 +269,7 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e_host, l_host = eng.local_energies(host_cfg)
-        if ws > 1:
-            vv = torch.tensor([float(B), e_host.real.sum(), (e_host.real ** 2).sum(), 0.0],
-                              dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_reduce(vv)
-            vv.cpu()
+        est_host = allreduce_stats(e_host, device=f"cuda:{local}")
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = float(np.median(e2e_times))
     if ws > 1:

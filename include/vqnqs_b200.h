@@ -82,6 +82,14 @@ int vqnqs_build_lattice(int lx, int ly, int periodic, int32_t* bonds, int cap);
 int vqnqs_zero_sz_samples(int n, int64_t start, int64_t count, uint64_t seed,
                           uint8_t* out);
 
+/* The reference's FLOP ledger for one connected set (flops::Ledger after
+ * local_energy_batch, proj/src/dedup.cpp:394-420 with opcost,
+ * proj/include/vqnqs/tensor.hpp:81-102) from its size K and the realised
+ * unique-row counts U[0..L] (L = blocks incl. a trailing half block).
+ * ADDS into ledger7. The engine fills ledgers this way. */
+int vqnqs_ledger_from_counts(const vqnqs_model_desc* d, int64_t K, const int64_t* U,
+                             int64_t* ledger7);
+
 /* ---- engine ---- */
 
 /* Uploads weights (float64, parameters() order) to `device`, converting to

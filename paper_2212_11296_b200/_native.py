@@ -45,6 +45,7 @@ SIGNATURES = {
                                     C.POINTER(P_F64)]),
     "vqnqs_build_lattice": (C.c_int, [C.c_int, C.c_int, C.c_int, P_I32, C.c_int]),
     "vqnqs_zero_sz_samples": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_uint64, P_U8]),
+    "vqnqs_ledger_from_counts": (C.c_int, [C.POINTER(ModelDesc), C.c_int64, P_I64, P_I64]),
     "vqnqs_gpu_create": (C.c_int, [C.POINTER(ModelDesc), C.POINTER(P_F64), C.c_int, C.c_int,
                                    C.c_int, C.POINTER(C.c_void_p)]),
     "vqnqs_gpu_set_hamiltonian": (C.c_int, [C.c_void_p, P_I32, C.c_int, C.c_int, C.c_int]),

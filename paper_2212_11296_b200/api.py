@@ -182,6 +182,17 @@ class Ledger:
             setattr(self, f, getattr(self, f) + getattr(o, f))
         return self
 
+    @staticmethod
+    def from_counts(cfg: ModelConfig, K: int, U) -> "Ledger":
+        """Ledger of one local_energy_batch from its connected-set size K and
+        unique-row counts U[0..L] (the engine's host-side recomputation)."""
+        u = np.ascontiguousarray(U, np.int64)
+        out = np.zeros(7, np.int64)
+        desc = N.desc_of(cfg)
+        N.check(N.lib().vqnqs_ledger_from_counts(C.byref(desc), int(K), N.ptr(u, C.c_int64),
+                                                 N.ptr(out, C.c_int64)))
+        return Ledger.from_array(out)
+
     def savings(self) -> Tuple[float, float]:
         """(total, quantized-ops) savings, proj/src/bench.cpp:110-114."""
         tot = self.total_dense() / max(1, self.total_dedup())

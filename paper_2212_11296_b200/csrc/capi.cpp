@@ -73,6 +73,15 @@ int vqnqs_zero_sz_samples(int n, int64_t start, int64_t count, uint64_t seed, ui
   });
 }
 
+int vqnqs_ledger_from_counts(const vqnqs_model_desc* d, int64_t K, const int64_t* U,
+                             int64_t* ledger7) {
+  return guarded([&] {
+    if (!d || !U || !ledger7) throw vqb::UsageError("null argument");
+    vqb::validate(*d);
+    vqb::ledger_add(*d, K, U, ledger7);
+  });
+}
+
 int vqnqs_gpu_create(const vqnqs_model_desc* d, const double* const* params, int n_params,
                      int precision, int device, vqnqs_handle** out) {
   return guarded([&] {

@@ -142,6 +142,7 @@ class EngineImpl {
   double prof[12] = {0};
   // arena
   int S_max = 256;
+  DBuf<int32_t> row_perm_;
   DBuf<int32_t> K_, Mact_, row_bond_, row_t1_, tok0_, lrow_, Ucnt_, I_a, I_b, code_, slot_,
       rep_of_, trep_, tuid_, g_code_;
   DBuf<int16_t> lpos_, upos_;
@@ -383,12 +384,12 @@ class EngineImpl {
     const int R1 = nb + 1;
     const int64_t R = int64_t(S) * R1;
     K_.ensure(S); attw_.ensure(S); Mact_.ensure(S); diag_.ensure(S); act_off_.ensure(S); tab_off_.ensure(S);
-    row_bond_.ensure(R); row_t1_.ensure(R); row_aoff_.ensure(R); tok0_.ensure(int64_t(S) * T);
+    row_bond_.ensure(R); row_perm_.ensure(R); row_t1_.ensure(R); row_aoff_.ensure(R); tok0_.ensure(int64_t(S) * T);
     Ucnt_.ensure(int64_t(L + 1) * S); Uoff_.ensure(int64_t(L + 1) * S); tot_.ensure(2 * (L + 2));
     int64_t* tot = tot_.p;  // [0] M total, [1] table total, [2+b] U_b total
     k_connected<<<(S * 32 + 127) / 128, 128, 0, st>>>(S, N, g, T, nb, d_cfg, d_bonds, K_.p, diag_.p,
                                                       row_bond_.p, row_t1_.p, row_aoff_.p, Mact_.p,
-                                                      tok0_.p, attw_.p);
+                                                      tok0_.p, attw_.p, row_perm_.p);
     k_scan<<<1, 1024, 0, st>>>(S, Mact_.p, act_off_.p, tot + 0, 0);
     k_scan<<<1, 1024, 0, st>>>(S, Mact_.p, tab_off_.p, tot + 1, 1);
     launches += 3;
@@ -452,8 +453,8 @@ class EngineImpl {
         if (b == 0) {
           tiles_.ensure(R);
           CK(cudaMemsetAsync(ntiles_.p, 0, sizeof(int32_t), st));
-          k_build_tiles<<<(S * 32 + 127) / 128, 128, 0, st>>>(S, R1, T, K_.p, row_t1_.p,
-                                                              act_off_.p, tiles_.p, ntiles_.p);
+          k_build_tiles<<<(S + 127) / 128, 128, 0, st>>>(S, R1, T, K_.p, row_t1_.p, row_perm_.p,
+                                                         act_off_.p, tiles_.p, ntiles_.p);
           ++launches;
         }
         const size_t asmem = AttnSmem(T).total + 1024;

@@ -42,7 +42,7 @@ __global__ void k_connected(int S, int N, int g, int T, int nb, const uint8_t* _
                             double* __restrict__ diag, int32_t* __restrict__ row_bond,
                             int32_t* __restrict__ row_t1, int64_t* __restrict__ row_aoff,
                             int32_t* __restrict__ Mact, int32_t* __restrict__ tok0,
-                            int64_t* __restrict__ attw) {
+                            int64_t* __restrict__ attw, int32_t* __restrict__ row_perm) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= S) return;
@@ -106,6 +106,68 @@ __global__ void k_connected(int S, int N, int g, int T, int nb, const uint8_t* _
     Mact[s] = (int32_t)aoff;
     attw[s] = aw;
   }
+  // Re-lay the rows' active regions in order of first changed token (stable
+  // counting sort by t1): rows that share t1 share their base-key range and
+  // suffix length, so attention tiles built in this order (row_perm) have
+  // tight live score ranges. Values are unaffected: unique rows are
+  // order-independent and U counts are order-invariant.
+  __shared__ int hist_all[4][1025];
+  __shared__ int sloc_all[4][1025];
+  int* hist = hist_all[(threadIdx.x >> 5) & 3];
+  int* sloc = sloc_all[(threadIdx.x >> 5) & 3];
+  for (int t = lane; t < T; t += 32) hist[t] = 0;
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int k0 = 1; k0 < nrows; k0 += 32) {
+    const int k = k0 + lane;
+    const bool valid = k < nrows;
+    const int t1 = valid ? row_t1[(int64_t)s * R1 + k] : T + lane;
+    const unsigned mk = __match_any_sync(0xffffffffu, t1);
+    const int rank_in = __popc(mk & lt);
+    const int basec = valid ? hist[t1] : 0;
+    __syncwarp();
+    if (valid && rank_in == 0) hist[t1] += __popc(mk);
+    __syncwarp();
+    if (valid) row_aoff[(int64_t)s * R1 + k] = basec + rank_in;  // rank, finalised below
+  }
+  __syncwarp();
+  // exclusive prefix over t1 buckets of (locations, rows)
+  {
+    const int per = (T + 31) / 32;
+    const int b = lane * per, e = min(T, b + per);
+    int locs = 0, rows = 0;
+    for (int t = b; t < e; ++t) {
+      locs += hist[t] * (T - t - 1);
+      rows += hist[t];
+    }
+    int il = locs, ir = rows;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int nl = __shfl_up_sync(0xffffffffu, il, o);
+      const int nr = __shfl_up_sync(0xffffffffu, ir, o);
+      if (lane >= o) {
+        il += nl;
+        ir += nr;
+      }
+    }
+    int rl = il - locs, rr = ir - rows;
+    for (int t = b; t < e; ++t) {
+      const int h = hist[t];
+      sloc[t] = rl;
+      hist[t] = rr;  // now: first layout row index (minus the base row) of bucket t
+      rl += h * (T - t - 1);
+      rr += h;
+    }
+  }
+  __syncwarp();
+  for (int k = 1 + lane; k < nrows; k += 32) {
+    const int64_t r = (int64_t)s * R1 + k;
+    const int t1 = row_t1[r];
+    const int rank = (int)row_aoff[r];
+    row_aoff[r] = T + sloc[t1] + (int64_t)rank * (T - t1 - 1);
+    row_perm[(int64_t)s * R1 + 1 + hist[t1] + rank] = k;
+  }
+  if (lane == 0) row_perm[(int64_t)s * R1] = 0;
 }
 
 // Exclusive scan of per-sample counts (single CTA). mode 1 scans hash-table

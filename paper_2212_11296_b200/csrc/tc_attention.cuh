@@ -45,6 +45,7 @@ struct AttnTile {
 // tiles of <= 128 locations, one thread per sample.
 __global__ void k_build_tiles(int S, int R1, int T, const int32_t* __restrict__ K,
                               const int32_t* __restrict__ row_t1,
+                              const int32_t* __restrict__ row_perm,
                               const int64_t* __restrict__ act_off, AttnTile* __restrict__ tiles,
                               int32_t* __restrict__ n_tiles) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -52,7 +53,8 @@ __global__ void k_build_tiles(int S, int R1, int T, const int32_t* __restrict__ 
   const int Ks = K[s];
   int cur = 0;
   int64_t start = act_off[s];
-  for (int k = 0; k < Ks; ++k) {
+  for (int i = 0; i < Ks; ++i) {  // rows in active-layout order (k_connected)
+    const int k = row_perm[(int64_t)s * R1 + i];
     const int n = k == 0 ? T : T - (row_t1[(int64_t)s * R1 + k] + 1);
     if (n <= 0) continue;
     if (cur + n > 128) {

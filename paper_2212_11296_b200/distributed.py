@@ -1,0 +1,70 @@
+"""Sample sharding across GPUs and the fill_stats collective.
+
+The local-energy path shards naturally by sample (every sample's connected
+set, dedup, attention and E_loc are independent: proj/src/dedup.cpp:394-420,
+SPEC.md:422), so one process per GPU evaluates its own block of samples with
+no data-path communication. The only collective reproduces fill_stats
+(proj/src/trainer.cpp:184-198): the energy mean, the unbiased variance of
+Re E_loc and its standard error over the whole batch, as two small fp64
+allreduces (sum; then the centred sum of squares, the same two-pass formula
+as the reference) over NCCL on GPUs or gloo on CPU.
+"""
+from __future__ import annotations
+
+import math
+from typing import Optional, Tuple
+
+import numpy as np
+
+from .api import VmcEstimate
+
+
+def shard_bounds(n_total: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous block of samples for `rank`: (start, count); the first
+    n_total % world ranks get one extra sample."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(n_total, world)
+    count = base + (1 if rank < extra else 0)
+    start = rank * base + min(rank, extra)
+    return start, count
+
+
+def allreduce_stats(e_local, device=None, group=None) -> VmcEstimate:
+    """fill_stats over all ranks' local energies (complex numpy array or a
+    torch float64 tensor of real parts)."""
+    import torch
+    import torch.distributed as dist
+    if isinstance(e_local, torch.Tensor):
+        re = e_local.to(torch.float64)
+        dev = re.device
+        im_sum = torch.zeros((), dtype=torch.float64, device=dev)
+    else:
+        arr = np.asarray(e_local)
+        dev = device if device is not None else "cpu"
+        re = torch.as_tensor(np.ascontiguousarray(arr.real), dtype=torch.float64, device=dev)
+        im_sum = torch.as_tensor(float(np.sum(arr.imag)), dtype=torch.float64, device=dev)
+    n = torch.tensor(float(re.numel()), dtype=torch.float64, device=dev)
+    v = torch.stack([n, re.sum(), im_sum])
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(v, group=group)
+    n_tot = float(v[0].item())
+    mean = float(v[1].item()) / n_tot
+    c = ((re - mean) ** 2).sum().reshape(1)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(c, group=group)
+    k = int(round(n_tot))
+    var = float(c.item()) / (k - 1) if k > 1 else 0.0
+    return VmcEstimate(mean, var, math.sqrt(var / k) if k else 0.0,
+                       np.zeros(0, complex))
+
+
+def local_energies_sharded(engine, batch_global, rank: int, world: int,
+                           group=None, device=None):
+    """Evaluate this rank's shard of a global batch on `engine` (a
+    LocalEnergyEngine on this rank's GPU) and return (E_loc shard, logpsi
+    shard, global VmcEstimate)."""
+    start, count = shard_bounds(len(batch_global), rank, world)
+    e, lpsi = engine.local_energies(np.asarray(batch_global)[start:start + count])
+    est = allreduce_stats(e, device=device, group=group)
+    return e, lpsi, est

@@ -1,0 +1,79 @@
+"""Generate the committed golden fixtures from the REFERENCE ITSELF.
+
+Runs the reference's own hot-path sources (oracle/_ref/libvqnqs_ref.so:
+proj/src/{flops,tensor,hamiltonian,model,dedup}.cpp compiled unmodified with
+the Eigen shim) on seeded inputs and writes small .npz fixtures:
+
+  golden_<case>.npz : samples, per-sample E_loc / logpsi, the ledger, and for
+                      the first few samples the taps (U counts, VQ codes,
+                      top-2 gaps, per-row log-probs).
+
+Needs /root/reference (dev container only). The fixtures travel with the repo;
+tests/test_oracle.py checks the C restatement (oracle/_port) against them.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+from oracle import RefLib  # noqa: E402
+from paper_2212_11296_b200.config import ModelConfig, workload  # noqa: E402
+
+CASES = {
+    # name: (workload or explicit cfg, lattice, bf16, n_samples, n_taps)
+    "c1_fp64": ("c1", None, False, 64, 8),
+    "c2_fp64": ("c2", None, False, 16, 4),
+    "c3_bf16": ("c3", None, True, 2, 2),
+    # reference test-suite shapes (proj/tests/test_dedup.cpp small_cfg):
+    # vq_heads=2, codebook 8, trailing half block, open 4x4 lattice
+    "small_open4x4": (ModelConfig(n_sites=16, group_size=2, d_hidden=16, n_heads=2,
+                                  n_blocks=1, trailing_half_block=True, vq_heads=2,
+                                  vq_codebook=8), ("grid", 4, 4), False, 32, 4),
+    "small_chain6_g3": (ModelConfig(n_sites=6, group_size=3, d_hidden=24, n_heads=2,
+                                    n_blocks=2, trailing_half_block=False, vq_heads=2,
+                                    vq_codebook=16), ("chain_periodic", 6, 0), False, 16, 4),
+}
+
+
+def main():
+    R = RefLib()
+    for name, (wl, lat, bf, ns, nt) in CASES.items():
+        if isinstance(wl, str):
+            w = workload(wl)
+            cfg, L = w.model, w.L
+            lat = ("grid_periodic", L, L)
+        else:
+            cfg = wl
+        R.set_bf16(bf)
+        m = R.model(cfg, 0, snap_bf16=bf)
+        h = R.hamiltonian(lat[0], lat[1], lat[2])
+        S = R.zero_sz_samples(cfg.n_sites, 0, ns, 1)
+        e_re, e_im, lpsi, led = m.local_energies(h, S, workers=os.cpu_count() or 4)
+        out = dict(samples=S, e_re=e_re, e_im=e_im, logpsi=lpsi, ledger=led,
+                   bonds=h.bonds(), bf16=np.array(bf),
+                   cfg=np.array([cfg.n_sites, cfg.group_size, cfg.d_hidden, cfg.n_heads,
+                                 cfg.n_blocks, int(cfg.trailing_half_block),
+                                 int(cfg.vq_enabled), cfg.vq_heads, cfg.vq_codebook]),
+                   vq_init_scale=np.array(cfg.vq_init_scale),
+                   lattice=np.array([{"grid": 1, "grid_periodic": 2, "chain": 0,
+                                      "chain_periodic": 3}[lat[0]], lat[1], lat[2]]))
+        params = m.params()
+        out["param_checksums"] = np.array([np.float64(p.sum()) for _, p in params])
+        out["param_first"] = np.array([p.reshape(-1)[0] for _, p in params])
+        for i in range(nt):
+            t = m.taps(h, S[i])
+            out[f"taps{i}_U"] = t.U
+            out[f"taps{i}_codes"] = t.codes
+            out[f"taps{i}_gaps"] = t.gaps
+            out[f"taps{i}_lp"] = t.lp
+        np.savez_compressed(os.path.join(HERE, f"golden_{name}.npz"), **out)
+        print(name, "E[:3]", e_re[:3], "ledger", led.tolist())
+
+
+if __name__ == "__main__":
+    main()
