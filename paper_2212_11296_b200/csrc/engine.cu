@@ -67,6 +67,7 @@ struct DBuf {
 struct DevBlock {
   float *ln1_g, *ln1_b, *bqkv, *bo, *ln2_g, *ln2_b, *b1, *b2, *cb32, *wn2;
   float wmax;
+  CUtensorMap tmB;                       // codebook tensor map (tcgen05 VQ)
   void *wqkv, *wo, *w1, *w2, *cbA;       // [in x out] row-major, operand type
   void *wqkvT, *woT, *w1T, *w2T;         // [out x in] (K-major) copies for tcgen05
 };
@@ -277,6 +278,7 @@ class EngineImpl {
         }
         B.wn2 = upload(wn2);
         B.wmax = float(wmax * (1.0 + 1e-6));
+        if (use_tc_vq) B.tmB = make_tmap_bf16(B.cbA, uint64_t(Q), uint64_t(d), 256);
       }
       B.ln2_g = upload_f(ln2g, d);
       B.ln2_b = upload_f(ln2b, d);
@@ -484,7 +486,7 @@ class EngineImpl {
                                                rr2_.p);
             ++launches;
           }
-          tc_vq(tot + 0, M, d, att_hi_.p, att_lo_.p, xn2_.p, rr2_.p, B.cbA, B.cb32, B.wn2, B.wmax, Q,
+          tc_vq(tot + 0, M, d, att_hi_.p, att_lo_.p, xn2_.p, rr2_.p, B.tmB, B.cb32, B.wn2, B.wmax, Q,
                 code_.p, d_rescored, st, sms);
         } else {
           const int LOCS = d > 384 ? 32 : 64;

@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
             const float d0 = v[j] - __low2float(h), d1 = v[j + 1] - __high2float(h);
             pl[j / 2] = tc::pack_bf16(d0, d1);
             const __nv_bfloat162 l = *reinterpret_cast<const __nv_bfloat162*>(&pl[j / 2]);
-            const float r0 = d0 - __low2float(l), r1 = d1 - __high2float(l);
+            const float r0 = __low2float(l), r1 = __high2float(l);  // |xl|^2 (tc_vq.cuh)
             xn2 = fmaf(v[j], v[j], fmaf(v[j + 1], v[j + 1], xn2));
             rr2 = fmaf(r0, r0, fmaf(r1, r1, rr2));
           }

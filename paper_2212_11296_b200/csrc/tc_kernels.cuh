@@ -91,7 +91,7 @@ __global__ void k_vq_prep(const int64_t* __restrict__ Mp, int d, const float* __
       const bf16 h = __float2bfloat16_rn(v);
       const float df = v - __bfloat162float(h);
       const bf16 l = __float2bfloat16_rn(df);
-      const float rr = df - __bfloat162float(l);
+      const float rr = __bfloat162float(l);  // |xl|^2 feeds the certified-argmin bound
       xh[r * d + c] = h;
       xl[r * d + c] = l;
       n2 = fmaf(v, v, n2);
@@ -106,8 +106,10 @@ __global__ void k_vq_prep(const int64_t* __restrict__ Mp, int d, const float* __
   }
 }
 
+// xh/xl: [Mcap x d] bf16 planes; tmB: the layer's codebook tensor map
+// (make_tmap_bf16(cbA, Q, d, 256)).
 inline void tc_vq(const int64_t* Mp, int64_t Mcap, int d, const bf16* xh, const bf16* xl,
-                  const float* xn2, const float* rr2, const void* cbA, const float* cb32,
+                  const float* xn2, const float* xl2, const CUtensorMap& tmB, const float* cb32,
                   const float* wn2, float wmax, int Q, int32_t* code,
                   unsigned long long* n_rescored, cudaStream_t st, int sms) {
   const size_t smem = tcv_smem_bytes(Q);
@@ -116,10 +118,12 @@ inline void tc_vq(const int64_t* Mp, int64_t Mcap, int d, const bf16* xh, const 
     cudaFuncSetAttribute(k_tc_vq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     attr = smem;
   }
+  const CUtensorMap tmA = make_tmap_bf16(xh, uint64_t(Mcap), uint64_t(d), 128);
+  const CUtensorMap tmL = make_tmap_bf16(xl, uint64_t(Mcap), uint64_t(d), 128);
   const int64_t tiles = (Mcap + 127) / 128;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
-  k_tc_vq<<<grid, TCV_THREADS, smem, st>>>(Mp, d, xh, xl, xn2, rr2, static_cast<const bf16*>(cbA),
-                                           cb32, wn2, wmax, Q, code, n_rescored);
+  k_tc_vq<<<grid, TCV_THREADS, smem, st>>>(tmA, tmL, tmB, Mp, d, xh, xl, xn2, xl2, cb32, wn2, wmax, Q,
+                                           code, n_rescored);
 }
 
 }  // namespace vqb

@@ -1,37 +1,42 @@
 // (c) Vector quantizer on tcgen05 with a certified argmin
 // (vq_apply_rows, proj/src/model.cpp:283-319; ties to the lowest index).
 //
-// Input per attention-output row x: its two-term bf16 split x = xh + xl + r
-// (xh = bf16(x), xl = bf16(x - xh), |r| <= 2^-18 |x|), |x|^2 and |r|^2, all
-// written by the attention epilogue. For 128 rows per tile:
-//   1. tensor cores accumulate acc_j = xh.W_j + xl.W_j for every codeword
-//      (W is bf16-exact: the bf16 configs snap weights to bf16) into up to
-//      512 TMEM columns per pass; A/B stream through a cp.async ring;
-//   2. D~_j = |W_j|^2 - 2 acc_j differs from D_j = |x - W_j|^2 - |x|^2 by at
-//      most E = 2(|r| + d 2^-23 |x|) max_j |W_j| + rounding slack;
-//   3. a streaming pass keeps every code with D~_j <= running min + 2E;
-//      a single survivor is the answer, otherwise the survivors are
-//      re-scored as sum_c ((xh_c + xl_c) - W_jc)^2 in double, c ascending —
-//      the reference's own arithmetic (proj/src/model.cpp:298-303) — and the
-//      lowest index wins (strict <, :304).
-// 512 threads: warp w drains TMEM lanes 32(w%4).. (its rows); the four
-// warpgroups split the code columns and merge candidates through smem.
+// Input per attention-output row x (written by the attention epilogue): the
+// two-term bf16 split x = xh + xl + r (xh = bf16(x), xl = bf16(x - xh), so
+// |r| <= 2^-8/(1-2^-8) |xl|), |x|^2 and |xl|^2. Warp-specialised persistent
+// kernel, 128 rows per tile:
+//   warp 0   TMA producer: A = xh, xl [128 x 64] and B = codebook[256 x 64]
+//            per K-block into a 3-stage SW128 ring (mbarrier full/empty);
+//   warp 1   MMA issuer: acc_j = xh . W_j + xl . W_j, 256 codes per
+//            accumulator, two TMEM accumulators (512 columns) so the
+//            epilogue of one code chunk overlaps the MMAs of the next;
+//   warps 2-9 epilogue (two warpgroups, 128 columns each): D~_j =
+//            |W_j|^2 - 2 acc_j is within E = 2(|r| + d 2^-23 |x|) max|W| +
+//            slack of the exact D_j(x) - |x|^2, so every code with
+//            D~_j <= running min + 2E is kept (<= 8 per warpgroup); a single
+//            survivor is the answer, otherwise survivors are re-scored as
+//            sum_c ((xh + xl)_c - W_jc)^2 in double, c ascending — the
+//            reference's own arithmetic (proj/src/model.cpp:298-303) — and the
+//            lowest index wins (strict <, :304).
+// W is bf16-exact (the bf16 configs snap weights to bf16).
 #pragma once
 
 #include "common.cuh"
 #include "tc_common.cuh"
+#include "tma.cuh"
 
 namespace vqb {
 
-constexpr int TCV_NC = 512;  // codes per pass (TMEM columns)
+constexpr int TCV_NCH = 256;  // codes per accumulator
+constexpr int TCV_STAGES = 3;
 constexpr int TCV_A_BYTES = 128 * 128;
-constexpr int TCV_STAGE_BYTES = 2 * TCV_A_BYTES + TCV_NC * 128;
-constexpr int TCV_STAGES = 2;
-constexpr int TCV_CAND = 4;
-constexpr int TCV_THREADS = 512;
+constexpr int TCV_B_BYTES = TCV_NCH * 128;
+constexpr int TCV_STAGE_BYTES = 2 * TCV_A_BYTES + TCV_B_BYTES;
+constexpr int TCV_CAND = 8;
+constexpr int TCV_THREADS = 320;  // producer warp, MMA warp, 8 epilogue warps
 
 inline size_t tcv_smem_bytes(int Q) {
-  return size_t(TCV_STAGES) * TCV_STAGE_BYTES + 1024 + 256 + size_t(Q) * 4 + 4 * 128 * 24 + 64;
+  return 1024 + size_t(TCV_STAGES) * TCV_STAGE_BYTES + 256 + size_t(Q) * 4 + 2 * 128 * 24 + 64;
 }
 
 __device__ __forceinline__ double vq_exact_d2(const bf16* __restrict__ xh,
@@ -56,178 +61,195 @@ __device__ __forceinline__ double vq_exact_d2(const bf16* __restrict__ xh,
   return s2;
 }
 
+// Candidate list of one row (lives in local memory; touched only on the rare
+// near-minimum codes, kept out of line so the streaming loop stays small).
+struct Cands {
+  float d[TCV_CAND];
+  int j[TCV_CAND];
+  int n;
+  int overflow;
+};
+
+__device__ __noinline__ void cand_add(Cands& C, float dt, int j, float thr) {
+  int w = 0;
+  for (int i = 0; i < C.n; ++i)
+    if (C.d[i] <= thr) {
+      C.d[w] = C.d[i];
+      C.j[w] = C.j[i];
+      ++w;
+    }
+  C.n = w;
+  if (w < TCV_CAND) {
+    C.d[w] = dt;
+    C.j[w] = j;
+    C.n = w + 1;
+  } else {
+    C.overflow = 1;
+  }
+}
+
+__device__ __forceinline__ void epi_bar() {  // the 256 epilogue threads
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
+    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmL,
+    const __grid_constant__ CUtensorMap tmB,
     const int64_t* __restrict__ Mp, int d, const bf16* __restrict__ xh,
-    const bf16* __restrict__ xl, const float* __restrict__ xn2g, const float* __restrict__ rr2g,
-    const bf16* __restrict__ cbA, const float* __restrict__ cb32,
-    const float* __restrict__ wn2_g, float wmax, int Q, int32_t* __restrict__ code,
-    unsigned long long* __restrict__ n_rescored) {
+    const bf16* __restrict__ xl, const float* __restrict__ xn2g, const float* __restrict__ xl2g,
+    const float* __restrict__ cb32, const float* __restrict__ wn2_g, float wmax, int Q,
+    int32_t* __restrict__ code, unsigned long long* __restrict__ n_rescored) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + TCV_STAGES * TCV_STAGE_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + TCV_STAGES);
-  float* wn2 = reinterpret_cast<float*>(smem + TCV_STAGES * TCV_STAGE_BYTES + 256);
-  float* red_min = wn2 + Q;                               // [4][128]
-  int* red_cnt = reinterpret_cast<int*>(red_min + 512);   // [4][128]
-  double* red_d = reinterpret_cast<double*>(red_cnt + 512);  // [4][128]
-  int* red_j = reinterpret_cast<int*>(red_d + 512);        // [4][128]
-  int* red_jf = red_j + 512;                               // [4][128]
+  uint8_t* tail = smem + TCV_STAGES * TCV_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tail);
+  uint64_t* empty = full + TCV_STAGES;
+  uint64_t* acc_full = empty + TCV_STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* wn2 = reinterpret_cast<float*>(tail + 256);
+  float* red_min = wn2 + Q;                                 // [2][128]
+  int* red_cnt = reinterpret_cast<int*>(red_min + 256);     // [2][128]
+  int* red_jf = red_cnt + 256;                              // [2][128]
+  double* red_d = reinterpret_cast<double*>(red_jf + 256);  // [2][128]
+  int* red_j = reinterpret_cast<int*>(red_d + 256);         // [2][128]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int row = tid & 127, part = tid >> 7;
   const int64_t M = *Mp;
+  const int KB = d / 64;
+  const int NCH = Q / TCV_NCH;
+  const int64_t n_tiles = (M + 127) / 128;
   if (tid == 0) {
-    for (int s = 0; s < TCV_STAGES; ++s) tc::mbar_init(&mbar[s], 1);
+    for (int s = 0; s < TCV_STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_empty[b], 8);
+    }
     tc::mbar_fence_init();
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmL);
+    tc::prefetch_tmap(&tmB);
   }
-  if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
   for (int j = tid; j < Q; j += TCV_THREADS) wn2[j] = wn2_g[j];
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = tc::smem_u32(smem);
-  constexpr uint32_t idesc = tc::make_idesc_bf16(128, 256);
-  const int KB = d / 64;
-  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-  uint32_t g = 0;
-  unsigned long long rescored = 0;
 
-  for (int64_t m0 = (int64_t)blockIdx.x * 128; m0 < M; m0 += (int64_t)gridDim.x * 128) {
-    const int64_t my = m0 + row;
-    const bool live = my < M;
-    const float xn = live ? sqrtf(xn2g[my]) : 0.f;
-    const float rn = live ? sqrtf(rr2g[my]) : 0.f;
-    const float E = 2.f * (rn * wmax + float(d) * 1.2e-7f * xn * wmax) +
-                    4e-7f * (wmax * wmax + 2.f * xn * wmax);
-    const float w2 = 2.f * E;
-    float run_min = INFINITY;
-    float cd[TCV_CAND];
-    int cj[TCV_CAND];
-    int nc = 0;
-    bool overflow = false;
-    for (int q0 = 0; q0 < Q; q0 += TCV_NC) {
-      const int NC = min(TCV_NC, Q - q0);
-      auto load = [&](int kb, uint32_t gg) {
-        const uint32_t s = gg % TCV_STAGES;
-        const uint32_t sa = sbase + s * TCV_STAGE_BYTES, sl = sa + TCV_A_BYTES,
-                       sb = sa + 2 * TCV_A_BYTES;
-        const int k0 = kb * 64;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {  // A hi/lo: 128 rows x 8 chunks each
-          const int e = tid + i * TCV_THREADS;
-          const int r = e >> 3, c = e & 7;
-          const bool ok = m0 + r < M;
-          const int64_t off = (ok ? (m0 + r) * d : 0) + k0 + c * 8;
-          tc::cp_async16_zfill(sa + tc::sw128_chunk(r, c), xh + off, ok);
-          tc::cp_async16_zfill(sl + tc::sw128_chunk(r, c), xl + off, ok);
-        }
-        for (int e = tid; e < NC * 8; e += TCV_THREADS) {  // B: NC codes x 8 chunks
-          const int r = e >> 3, c = e & 7;
-          tc::cp_async16(sb + tc::sw128_chunk(r, c), cbA + (int64_t)(q0 + r) * d + k0 + c * 8);
-        }
-      };
-      {
-        const uint32_t gg = g;
-        if (gg >= TCV_STAGES) tc::mbar_wait(&mbar[gg % TCV_STAGES], ((gg / TCV_STAGES) - 1) & 1);
-        load(0, gg);
-        tc::cp_async_commit();
-      }
-      for (int kb = 0; kb < KB; ++kb) {
-        if (kb + 1 < KB) {
-          const uint32_t gg = g + kb + 1;
-          if (gg >= TCV_STAGES) tc::mbar_wait(&mbar[gg % TCV_STAGES], ((gg / TCV_STAGES) - 1) & 1);
-          load(kb + 1, gg);
-        }
-        tc::cp_async_commit();
-        tc::cp_async_wait<1>();
-        tc::fence_proxy_async();
-        __syncthreads();
-        if (tid == 0) {
-          tc::fence_after();
-          const uint32_t s = (g + kb) % TCV_STAGES;
-          const uint32_t sa = sbase + s * TCV_STAGE_BYTES, sl = sa + TCV_A_BYTES,
-                         sb = sa + 2 * TCV_A_BYTES;
-          for (int half = 0; half < NC / 256; ++half) {
-            const uint32_t bb = sb + half * 256 * 128;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc::mma_bf16(tmem + half * 256, tc::make_desc_sw128(sa + k * 32),
-                           tc::make_desc_sw128(bb + k * 32), idesc, (kb | k) != 0);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc::mma_bf16(tmem + half * 256, tc::make_desc_sw128(sl + k * 32),
-                           tc::make_desc_sw128(bb + k * 32), idesc, 1u);
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        for (int c = 0; c < NCH; ++c)
+          for (int kb = 0; kb < KB; ++kb, ++it) {
+            const uint32_t s = it % TCV_STAGES;
+            if (it >= TCV_STAGES) tc::mbar_wait(&empty[s], ((it / TCV_STAGES) - 1) & 1);
+            const uint32_t sa = sbase + s * TCV_STAGE_BYTES;
+            const uint32_t fb = tc::smem_u32(&full[s]);
+            tc::mbar_expect_tx(fb, TCV_STAGE_BYTES);
+            tc::tma_load_2d(sa, &tmA, kb * 64, int(t * 128), fb);
+            tc::tma_load_2d(sa + TCV_A_BYTES, &tmL, kb * 64, int(t * 128), fb);
+            tc::tma_load_2d(sa + 2 * TCV_A_BYTES, &tmB, kb * 64, c * TCV_NCH, fb);
           }
-          tc::mma_commit(&mbar[s]);
-        }
       }
-      {
-        const uint32_t gl = g + KB - 1;
-        tc::mbar_wait(&mbar[gl % TCV_STAGES], (gl / TCV_STAGES) & 1);
-      }
-      g += KB;
-      tc::fence_after();
-      // ---- streaming candidate pass: this warpgroup's 32-column chunks
-      for (int c0 = part * 32; c0 < NC; c0 += 128) {
-        float v[32];
-        tc::tmem_ld32(trow + c0, v);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float dt = fmaf(-2.f, v[j], wn2[q0 + c0 + j]);
-          if (dt <= run_min + w2) {
-            run_min = fminf(run_min, dt);
-            int w = 0;
-#pragma unroll
-            for (int i = 0; i < TCV_CAND; ++i) {
-              if (i < nc && cd[i] <= run_min + w2) {
-#pragma unroll
-                for (int t = 0; t < TCV_CAND; ++t)
-                  if (t == w) {
-                    cd[t] = cd[i];
-                    cj[t] = cj[i];
-                  }
-                ++w;
-              }
-            }
-            nc = w;
-            if (nc < TCV_CAND) {
-#pragma unroll
-              for (int t = 0; t < TCV_CAND; ++t)
-                if (t == nc) {
-                  cd[t] = dt;
-                  cj[t] = q0 + c0 + j;
-                }
-              ++nc;
-            } else {
-              overflow = true;
-            }
-          }
-        }
-      }
-      tc::fence_before();
-      __syncthreads();
     }
-    // ---- merge the four warpgroups' candidates
-    red_min[part * 128 + row] = run_min;
-    __syncthreads();
-    const float gmin = fminf(fminf(red_min[row], red_min[128 + row]),
-                             fminf(red_min[256 + row], red_min[384 + row]));
-    int mine = 0, jfirst = 0x7fffffff;
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::make_idesc_bf16(128, TCV_NCH);
+      uint32_t it = 0, acc = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        for (int c = 0; c < NCH; ++c, ++acc) {
+          const uint32_t b = acc & 1;
+          if (acc >= 2) tc::mbar_wait(&acc_empty[b], ((acc >> 1) - 1) & 1);
+          tc::fence_after();
+          for (int kb = 0; kb < KB; ++kb, ++it) {
+            const uint32_t s = it % TCV_STAGES;
+            tc::mbar_wait(&full[s], (it / TCV_STAGES) & 1);
+            tc::fence_after();
+            const uint32_t sa = sbase + s * TCV_STAGE_BYTES;
 #pragma unroll
-    for (int i = 0; i < TCV_CAND; ++i)
-      if (i < nc && cd[i] <= gmin + w2) {
-        ++mine;
-        jfirst = min(jfirst, cj[i]);
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t bdesc = tc::make_desc_sw128(sa + 2 * TCV_A_BYTES + k * 32);
+              tc::mma_bf16(tmem + b * TCV_NCH, tc::make_desc_sw128(sa + k * 32), bdesc, idesc,
+                           (kb | k) != 0);
+              tc::mma_bf16(tmem + b * TCV_NCH, tc::make_desc_sw128(sa + TCV_A_BYTES + k * 32),
+                           bdesc, idesc, 1u);
+            }
+            tc::mma_commit(&empty[s]);
+          }
+          tc::mma_commit(&acc_full[b]);
+        }
       }
-    red_cnt[part * 128 + row] = overflow ? 1000 : mine;
-    red_jf[part * 128 + row] = jfirst;
-    __syncthreads();
-    const int total = red_cnt[row] + red_cnt[128 + row] + red_cnt[256 + row] + red_cnt[384 + row];
-    {
-      // exact re-scoring when more than one code survives: each warpgroup
-      // over its own survivors (or, after an overflow, a quarter of all codes)
+    }
+  } else {
+    // ---------------- epilogue: 8 warps, warp w drains TMEM lanes 32 (w % 4)
+    const int row = (warp & 3) * 32 + lane;
+    const int part = (warp - 2) >> 2;  // 0 or 1: columns [128 part, 128 part + 128)
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    uint32_t acc = 0;
+    unsigned long long rescored = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int64_t my = t * 128 + row;
+      const bool live = my < M;
+      const float xn = live ? sqrtf(xn2g[my]) : 0.f;
+      const float xln = live ? sqrtf(xl2g[my]) : 0.f;
+      // |r| <= 2^-8 / (1 - 2^-8) |xl|: the residual of the two-term split
+      const float E = 2.f * (0.00393f * xln * wmax + float(d) * 1.2e-7f * xn * wmax) +
+                      4e-7f * (wmax * wmax + 2.f * xn * wmax);
+      const float w2 = 2.f * E;
+      float run_min = INFINITY;
+      Cands C;
+      C.n = 0;
+      C.overflow = 0;
+      for (int c = 0; c < NCH; ++c, ++acc) {
+        const uint32_t b = acc & 1;
+        tc::mbar_wait(&acc_full[b], (acc >> 1) & 1);
+        tc::fence_after();
+        for (int c0 = part * 128; c0 < part * 128 + 128; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(trow + b * TCV_NCH + c0, v);
+          tc::tmem_wait_ld();
+          const int jbase = c * TCV_NCH + c0;
+          float vmin = INFINITY;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v[j] = fmaf(-2.f, v[j], wn2[jbase + j]);
+            vmin = fminf(vmin, v[j]);
+          }
+          if (vmin <= run_min + w2) {  // rare once the running minimum settles
+            run_min = fminf(run_min, vmin);
+            const float thr = run_min + w2;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (v[j] <= thr) cand_add(C, v[j], jbase + j, thr);
+          }
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&acc_empty[b]));
+      }
+      // ---- merge the two warpgroups' survivors for this row
+      red_min[part * 128 + row] = run_min;
+      epi_bar();
+      const float gmin = fminf(red_min[row], red_min[128 + row]);
+      int mine = 0, jfirst = 0x7fffffff;
+#pragma unroll 1
+      for (int i = 0; i < C.n; ++i)
+        if (C.d[i] <= gmin + w2) {
+          ++mine;
+          jfirst = min(jfirst, C.j[i]);
+        }
+      red_cnt[part * 128 + row] = C.overflow ? 1000 : mine;
+      red_jf[part * 128 + row] = jfirst;
+      epi_bar();
+      const int total = red_cnt[row] + red_cnt[128 + row];
       double best = INFINITY;
       int jb = 0x7fffffff;
       if (live && total != 1) {
@@ -235,18 +257,18 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
         const bf16* xlr = xl + my * d;
         if (total < 1000) {
 #pragma unroll 1
-          for (int i = 0; i < TCV_CAND; ++i)
-            if (i < nc && cd[i] <= gmin + w2) {
-              const double s2 = vq_exact_d2(xhr, xlr, cb32 + (int64_t)cj[i] * d, d);
+          for (int i = 0; i < C.n; ++i)
+            if (C.d[i] <= gmin + w2) {
+              const double s2 = vq_exact_d2(xhr, xlr, cb32 + (int64_t)C.j[i] * d, d);
               ++rescored;
-              if (s2 < best || (s2 == best && cj[i] < jb)) {
+              if (s2 < best || (s2 == best && C.j[i] < jb)) {
                 best = s2;
-                jb = cj[i];
+                jb = C.j[i];
               }
             }
         } else {
 #pragma unroll 1
-          for (int j = part; j < Q; j += 4) {
+          for (int j = part; j < Q; j += 2) {
             const double s2 = vq_exact_d2(xhr, xlr, cb32 + (int64_t)j * d, d);
             ++rescored;
             if (s2 < best || (s2 == best && j < jb)) {
@@ -258,35 +280,28 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
       }
       red_d[part * 128 + row] = best;
       red_j[part * 128 + row] = jb;
-    }
-    __syncthreads();
-    if (part == 0 && live) {
-      int j;
-      if (total == 1) {
-        j = min(min(red_jf[row], red_jf[128 + row]), min(red_jf[256 + row], red_jf[384 + row]));
-      } else {
-        double b = red_d[row];
-        j = red_j[row];
-        for (int p = 1; p < 4; ++p) {
-          const double v = red_d[p * 128 + row];
-          const int vj = red_j[p * 128 + row];
-          if (v < b || (v == b && vj < j)) {
-            b = v;
-            j = vj;
-          }
+      epi_bar();
+      if (part == 0 && live) {
+        int j;
+        if (total == 1) {
+          j = min(red_jf[row], red_jf[128 + row]);
+        } else {
+          const double b0 = red_d[row], b1 = red_d[128 + row];
+          const int j0 = red_j[row], j1 = red_j[128 + row];
+          j = (b1 < b0 || (b1 == b0 && j1 < j0)) ? j1 : j0;
         }
+        code[my] = j;
       }
-      code[my] = j;
+      epi_bar();
     }
-    __syncthreads();
-  }
-  if (n_rescored) {
+    if (n_rescored) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rescored += __shfl_xor_sync(0xffffffffu, rescored, o);
-    if (lane == 0) atomicAdd(n_rescored, rescored);
+      for (int o = 16; o > 0; o >>= 1) rescored += __shfl_xor_sync(0xffffffffu, rescored, o);
+      if (lane == 0) atomicAdd(n_rescored, rescored);
+    }
   }
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
 }  // namespace vqb
