@@ -195,22 +195,25 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       tc::fence_proxy_async();
       __syncthreads();
       const int kb_base = (s_amax + 15) & ~15;  // base keys any row of the tile uses
+      auto issue_scores = [&](int hq) {
+        const uint32_t qoff = (uint32_t)(hq * dh * 2);  // head offset inside the 128-B row
+        const uint32_t idS_b = tc::make_idesc_bf16(128, kb_base > 0 ? kb_base : 16);
+        const uint32_t idS_o = tc::make_idesc_bf16(128, 128);
+        for (int k = 0; k < dh / 16; ++k) {
+          if (kb_base > 0)
+            tc::mma_bf16(tmem + TS_BASE, tc::make_desc_sw128(sb + L.q + qoff + k * 32),
+                         tc::make_desc_sw128(sb + L.kbase + qoff + k * 32), idS_b, k != 0);
+          tc::mma_bf16(tmem + TS_OWN, tc::make_desc_sw128(sb + L.q + qoff + k * 32),
+                       tc::make_desc_sw128(sb + L.kown + qoff + k * 32), idS_o, k != 0);
+        }
+        tc::mma_commit(&mbar[0]);
+      };
+      if (tid == 0) {
+        tc::fence_after();
+        issue_scores(0);
+      }
       for (int hh = 0; hh < hpg; ++hh) {
         const uint32_t koff = (uint32_t)(hh * dh * 2);  // head offset inside the 128-B row
-        // ---- scores
-        if (tid == 0) {
-          tc::fence_after();
-          const uint32_t idS_b = tc::make_idesc_bf16(128, kb_base > 0 ? kb_base : 16);
-          const uint32_t idS_o = tc::make_idesc_bf16(128, 128);
-          for (int k = 0; k < dh / 16; ++k) {
-            if (kb_base > 0)
-              tc::mma_bf16(tmem + TS_BASE, tc::make_desc_sw128(sb + L.q + koff + k * 32),
-                           tc::make_desc_sw128(sb + L.kbase + koff + k * 32), idS_b, k != 0);
-            tc::mma_bf16(tmem + TS_OWN, tc::make_desc_sw128(sb + L.q + koff + k * 32),
-                         tc::make_desc_sw128(sb + L.kown + koff + k * 32), idS_o, k != 0);
-          }
-          tc::mma_commit(&mbar[0]);
-        }
         tc::mbar_wait(&mbar[0], ph_s);
         ph_s ^= 1;
         tc::fence_after();
@@ -265,6 +268,11 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         __syncthreads();
         tc::fence_after();
         const float inv = 1.f / (((red2[0][row] + red2[1][row]) + red2[2][row]) + red2[3][row]);
+        // P is rewritten only after the previous head's value MMA consumed it
+        if (hh > 0) {
+          tc::mbar_wait(&mbar[1], ph_o);
+          ph_o ^= 1;
+        }
         // ---- pass 3: normalised bf16 probabilities into the P tiles
         for (int c0 = part * 16; c0 < kb_base; c0 += 64) {
           uint32_t pk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -300,6 +308,9 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         // ---- O_h = P_base V_base + P_own V_own  (V is the MN-major B operand)
         if (tid == 0) {
           tc::fence_after();
+          // the next head's scores first (S was fully read before the barrier
+          // above), so its softmax overlaps this head's value MMA
+          if (hh + 1 < hpg) issue_scores(hh + 1);
           const uint32_t idO = tc::make_idesc_bf16(128, dh) | (1u << 16);
           int first = 1;
           for (int k16 = 0; k16 < kb_base; k16 += 16) {
@@ -320,12 +331,10 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           }
           tc::mma_commit(&mbar[1]);
         }
-        // next head's scores overwrite S only after everyone read it (barrier
-        // above); P is rewritten only after O has consumed it
-        tc::mbar_wait(&mbar[1], ph_o);
-        ph_o ^= 1;
-        tc::fence_after();
       }
+      tc::mbar_wait(&mbar[1], ph_o);  // the group's last value MMA
+      ph_o ^= 1;
+      tc::fence_after();
       // ---- drain the group's O: warpgroup `part` takes columns [16 part, 16 part + 16)
       {
         float v[16];
