@@ -66,6 +66,7 @@ struct DBuf {
 
 struct DevBlock {
   float *ln1_g, *ln1_b, *bqkv, *bo, *ln2_g, *ln2_b, *b1, *b2, *cb32, *wn2;
+  float* pwo;  // per-code continuation table [Q x d]: code_j Wo + bo
   float wmax;
   CUtensorMap tmB;                       // codebook tensor map (tcgen05 VQ)
   void *wqkv, *wo, *w1, *w2, *cbA;       // [in x out] row-major, operand type
@@ -305,6 +306,33 @@ class EngineImpl {
     head_w = upload_op(std::vector<double>(params[i], params[i] + (size_t)d * V));
     ++i;
     head_b = upload_f(nxt(), V);
+    // Per-code continuation tables: o_j = code_j Wo + bo for every codeword,
+    // with the same GEMM (and so the same per-row arithmetic) the per-row
+    // continuation would run — the values are bit-identical, and the Wo GEMM
+    // leaves the per-step path (hard part 7).
+    {
+      int64_t* dQ = nullptr;
+      float* zeros = nullptr;
+      CK(cudaMalloc(&dQ, sizeof(int64_t)));
+      const int64_t q64 = Q;
+      CK(cudaMemcpy(dQ, &q64, sizeof(int64_t), cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&zeros, size_t(Q) * d * sizeof(float)));
+      CK(cudaMemset(zeros, 0, size_t(Q) * d * sizeof(float)));
+      for (auto& B : blk) {
+        CK(cudaMalloc(&B.pwo, size_t(Q) * d * sizeof(float)));
+        allocs.push_back(B.pwo);
+        if (prec == VQNQS_PREC_BF16)
+          gemm<bf16>(dQ, Q, d, d, B.cbA, d, nullptr, B.wo, B.woT, B.bo, B.pwo, d, EPI_RESID, zeros,
+                     d, nullptr, own);
+        else
+          gemm<float>(dQ, Q, d, d, B.cbA, d, nullptr, B.wo, B.woT, B.bo, B.pwo, d, EPI_RESID,
+                      zeros, d, nullptr, own);
+      }
+      CK(cudaStreamSynchronize(own));
+      CK(cudaGetLastError());
+      cudaFree(dQ);
+      cudaFree(zeros);
+    }
   }
 
   ~EngineImpl() {
@@ -535,9 +563,9 @@ class EngineImpl {
       launches += 3;
       const int64_t* Mn = tot + 3 + b;
       // continuation (proj/src/dedup.cpp:246-267): y = r + (code_row Wo + bo)
-      gemm<TA>(Mn, M, d, d, B.cbA, d, g_code_.p, B.wo, B.woT, B.bo, y_.p, d, EPI_RESID, xcur, d,
-               g_res_.p, st);
-      k_layernorm<TA><<<lnGrid, 256, 0, st>>>(Mn, d, y_.p, B.ln2_g, B.ln2_b, h);
+      // from the per-code table, fused with LN2
+      k_cont_ln<TA><<<lnGrid, 256, 0, st>>>(Mn, d, xcur, g_res_.p, g_code_.p, B.pwo, B.ln2_g,
+                                            B.ln2_b, y_.p, h);
       ++launches;
       gemm<TA>(Mn, M, 4 * d, d, h, d, nullptr, B.w1, B.w1T, B.b1, f1, 4 * d, EPI_GELU, nullptr, 0,
                nullptr, st);

@@ -386,6 +386,43 @@ __global__ void k_layernorm(const int64_t* __restrict__ Mp, int d, const float* 
   }
 }
 
+// Continuation head (proj/src/dedup.cpp:255-262) on the U_{b+1} new unique
+// rows: y = r + o with r the block-input residual row and o = code_row Wo + bo
+// read from the per-code table pwo (computed once per model by the same GEMM,
+// so each row's o is bit-identical to a per-row product), then LN2(y).
+// One warp per row; y is kept for the W2 residual.
+template <typename TA>
+__global__ void k_cont_ln(const int64_t* __restrict__ Mp, int d, const float* __restrict__ x,
+                          const int64_t* __restrict__ g_res, const int32_t* __restrict__ g_code,
+                          const float* __restrict__ pwo, const float* __restrict__ gam,
+                          const float* __restrict__ bet, float* __restrict__ y,
+                          TA* __restrict__ out) {
+  const int64_t M = *Mp;
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
+    const float* xr = x + g_res[r] * d;
+    const float* pr = pwo + (int64_t)g_code[r] * d;
+    float* yr = y + r * d;
+    double s = 0.0;
+    for (int c = lane; c < d; c += 32) {
+      const float v = xr[c] + pr[c];
+      yr[c] = v;
+      s += v;
+    }
+    const double mean = warp_sum(s) / d;
+    double q = 0.0;
+    for (int c = lane; c < d; c += 32) {
+      const double t = yr[c] - mean;
+      q += t * t;
+    }
+    const double var = warp_sum(q) / d;
+    const double rstd = 1.0 / sqrt(var + 1e-5);
+    for (int c = lane; c < d; c += 32)
+      out[r * d + c] = from_f<TA>((float)((yr[c] - mean) * rstd * gam[c] + bet[c]));
+  }
+}
+
 // For each new unique row (global id g): which codebook row and which
 // residual row it concatenates (requantize's V' = [code row || residual row],
 // proj/src/dedup.cpp:176-184), and its token position.
