@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "tc_common.cuh"
+#include "tma.cuh"
 
 namespace vqb {
 
@@ -162,6 +163,154 @@ __global__ void __launch_bounds__(128, 1) k_tc_gemm(
   }
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem, BN < 32 ? 32 : BN);
+}
+
+// Warp-specialised persistent variant for contiguous A (QKV, W1, W2 and the
+// per-code table): warp 0 issues TMA for A [128 x 64] and W^T [BN x 64]
+// K-blocks into a 4-stage ring, warp 1 issues tcgen05.mma into one of two
+// BN-column TMEM accumulators, warps 2-9 (two warpgroups, BN/2 columns each)
+// drain the other accumulator through the fused epilogue, so loads, MMAs and
+// epilogues of consecutive tiles overlap.
+constexpr int TCW_STAGES = 4;
+constexpr int TCW_THREADS = 320;
+
+template <int BN>
+constexpr size_t tcw_smem_bytes() {
+  return 1024 + size_t(TCW_STAGES) * (128 * 128 + BN * 128) + 256;
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(TCW_THREADS, 1) k_tc_gemm_ws(
+    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+    const int64_t* __restrict__ Mp, int N, int K, const float* __restrict__ bias,
+    void* __restrict__ out, int ldo, const float* __restrict__ resid, int ldr) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  constexpr uint32_t A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TCW_STAGES * STAGE);
+  uint64_t* empty = full + TCW_STAGES;
+  uint64_t* acc_full = empty + TCW_STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t M = *Mp;
+  const int64_t tilesM = (M + 127) / 128;
+  const int tilesN = N / BN;
+  const int64_t n_tiles = tilesM * tilesN;
+  const int KB = K / 64;
+  if (tid == 0) {
+    for (int s = 0; s < TCW_STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_empty[b], 8);
+    }
+    tc::mbar_fence_init();
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmW);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = tc::smem_u32(smem);
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int m0 = int((t / tilesN) * 128), n0 = int(t % tilesN) * BN;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const uint32_t s = it % TCW_STAGES;
+          if (it >= TCW_STAGES) tc::mbar_wait(&empty[s], ((it / TCW_STAGES) - 1) & 1);
+          const uint32_t sa = sbase + s * STAGE;
+          const uint32_t fb = tc::smem_u32(&full[s]);
+          tc::mbar_expect_tx(fb, STAGE);
+          tc::tma_load_2d(sa, &tmA, kb * 64, m0, fb);
+          tc::tma_load_2d(sa + A_BYTES, &tmW, kb * 64, n0, fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::make_idesc_bf16(128, BN);
+      uint32_t it = 0, acc = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++acc) {
+        const uint32_t b = acc & 1;
+        if (acc >= 2) tc::mbar_wait(&acc_empty[b], ((acc >> 1) - 1) & 1);
+        tc::fence_after();
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const uint32_t s = it % TCW_STAGES;
+          tc::mbar_wait(&full[s], (it / TCW_STAGES) & 1);
+          tc::fence_after();
+          const uint32_t sa = sbase + s * STAGE;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc::mma_bf16(tmem + b * BN, tc::make_desc_sw128(sa + k * 32),
+                         tc::make_desc_sw128(sa + A_BYTES + k * 32), idesc, (kb | k) != 0);
+          tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(&acc_full[b]);
+      }
+    }
+  } else {
+    const int row = (warp & 3) * 32 + lane;
+    const int part = (warp - 2) >> 2;  // columns [part*BN/2, part*BN/2 + BN/2)
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    uint32_t acc = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++acc) {
+      const uint32_t b = acc & 1;
+      const int64_t m = (t / tilesN) * 128 + row;
+      const int n0 = int(t % tilesN) * BN;
+      tc::mbar_wait(&acc_full[b], (acc >> 1) & 1);
+      tc::fence_after();
+      for (int c0 = part * (BN / 2); c0 < (part + 1) * (BN / 2); c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(trow + b * BN + c0, v);
+        tc::tmem_wait_ld();
+        if (m < M) {
+          const int n = n0 + c0;
+          if (EPI == EPI_RESID) {
+            float* o = static_cast<float*>(out) + m * ldo + n;
+            const float* rs = resid + m * ldr + n;
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+              const float4 r4 = *reinterpret_cast<const float4*>(rs + j);
+              const float4 b4 = *reinterpret_cast<const float4*>(bias + n + j);
+              float4 o4;
+              o4.x = r4.x + (v[j] + b4.x);
+              o4.y = r4.y + (v[j + 1] + b4.y);
+              o4.z = r4.z + (v[j + 2] + b4.z);
+              o4.w = r4.w + (v[j + 3] + b4.w);
+              *reinterpret_cast<float4*>(o + j) = o4;
+            }
+          } else {
+            uint32_t pk[8];
+#pragma unroll
+            for (int j = 0; j < 16; j += 2) {
+              float a = v[j] + bias[n + j], c = v[j + 1] + bias[n + j + 1];
+              if (EPI == EPI_GELU) {
+                a = gelu_f(a);
+                c = gelu_f(c);
+              }
+              pk[j / 2] = tc::pack_bf16(a, c);
+            }
+            uint4* o = reinterpret_cast<uint4*>(static_cast<bf16*>(out) + m * ldo + n);
+            o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&acc_empty[b]));
+    }
+  }
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 2 * BN < 32 ? 32 : 2 * BN);
 }
 
 }  // namespace vqb

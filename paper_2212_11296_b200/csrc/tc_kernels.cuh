@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -58,12 +59,59 @@ inline void launch_tc_gemm_bn(const int64_t* Mp, int64_t Mcap, int N, int K, con
   }
 }
 
+template <int BN, int EPI>
+inline void launch_tc_gemm_ws(const int64_t* Mp, int64_t Mcap, int N, int K, const bf16* A,
+                              int lda, const bf16* WT, const float* bias, void* out, int ldo,
+                              const float* resid, int ldr, cudaStream_t st, int sms) {
+  const size_t smem = tcw_smem_bytes<BN>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tc_gemm_ws<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    attr = true;
+  }
+  const CUtensorMap tmA = make_tmap_bf16(A, uint64_t(Mcap), uint64_t(K), 128, uint64_t(lda));
+  const CUtensorMap tmW = make_tmap_bf16(WT, uint64_t(N), uint64_t(K), BN);
+  const int64_t tiles = ((Mcap + 127) / 128) * (N / BN);
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
+  k_tc_gemm_ws<BN, EPI><<<grid, TCW_THREADS, smem, st>>>(tmA, tmW, Mp, N, K, bias, out, ldo,
+                                                         resid, ldr);
+}
+
+template <int BN>
+inline void launch_tc_gemm_ws_bn(const int64_t* Mp, int64_t Mcap, int N, int K, const bf16* A,
+                                 int lda, const bf16* WT, const float* bias, void* out, int ldo,
+                                 int epi, const float* resid, int ldr, cudaStream_t st, int sms) {
+  if (epi == EPI_STORE)
+    launch_tc_gemm_ws<BN, EPI_STORE>(Mp, Mcap, N, K, A, lda, WT, bias, out, ldo, resid, ldr, st,
+                                     sms);
+  else if (epi == EPI_GELU)
+    launch_tc_gemm_ws<BN, EPI_GELU>(Mp, Mcap, N, K, A, lda, WT, bias, out, ldo, resid, ldr, st,
+                                    sms);
+  else
+    launch_tc_gemm_ws<BN, EPI_RESID>(Mp, Mcap, N, K, A, lda, WT, bias, out, ldo, resid, ldr, st,
+                                     sms);
+}
+
 inline void tc_gemm(const int64_t* Mp, int64_t Mcap, int N, int K, const void* A, int lda,
                     const int32_t* gA, const void* WT, const float* bias, void* out, int ldo,
                     int epi, const float* resid, int ldr, const int64_t* gR, cudaStream_t st,
                     int sms) {
   const bf16* a = static_cast<const bf16*>(A);
   const bf16* w = static_cast<const bf16*>(WT);
+  if (!gA && !gR && !getenv("VQNQS_GEMM_V1")) {
+    // warp-specialised TMA path (contiguous A rows, identity residual rows)
+    if (N % 256 == 0)
+      launch_tc_gemm_ws_bn<256>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, epi, resid, ldr, st,
+                                sms);
+    else if (N % 128 == 0)
+      launch_tc_gemm_ws_bn<128>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, epi, resid, ldr, st,
+                                sms);
+    else
+      launch_tc_gemm_ws_bn<64>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, epi, resid, ldr, st,
+                               sms);
+    return;
+  }
   if (N % 256 == 0)
     launch_tc_gemm_bn<256>(Mp, Mcap, N, K, a, lda, gA, w, bias, out, ldo, epi, resid, ldr, gR, st,
                            sms);

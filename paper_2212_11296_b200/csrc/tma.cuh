@@ -17,7 +17,7 @@ namespace vqb {
 
 // bf16 matrix [rows x cols] row-major (cols contiguous), box [box_rows x 64].
 inline CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols,
-                                  uint32_t box_rows) {
+                                  uint32_t box_rows, uint64_t pitch_elems = 0) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -30,7 +30,7 @@ inline CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols
   }
   CUtensorMap m;
   const cuuint64_t dims[2] = {cols, rows};
-  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint64_t strides[1] = {(pitch_elems ? pitch_elems : cols) * 2};
   const cuuint32_t box[2] = {64, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
