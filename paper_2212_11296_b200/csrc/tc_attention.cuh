@@ -18,9 +18,10 @@
 // All operands are staged with cp.async per 64-wide head group as SW128
 // tiles [rows x 64]: Q/K are K-major operands; V, staged the same way
 // (key rows, 64 head-dims contiguous), is the MN-major B operand of the value
-// product, so nothing is transposed. Softmax: three TMEM passes over only
-// the warp's live columns (max; exp2 + sum, exponentials stored back to
-// TMEM; normalise + bf16 into the P tiles) so each score costs one MUFU op.
+// product, so nothing is transposed. Softmax: ONE TMEM pass loads the warp's
+// live score columns into registers (4 x 16 per thread); max, exp2 + sum and
+// the normalised bf16 P tiles are computed from registers, and the next
+// head's score MMA is issued as soon as every warp has loaded its scores.
 // TMEM: S_base | S_own | O(group) = T_pad + 128 + 64 <= 512 columns.
 //
 // Outputs per active location: the attention row x as its two-term bf16
@@ -217,100 +218,85 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         tc::mbar_wait(&mbar[0], ph_s);
         ph_s ^= 1;
         tc::fence_after();
-        // ---- pass 1: row max; warpgroup `part` owns 16-column chunks part, part+4, ...
+        // ---- the warp's live score chunks go to registers in ONE TMEM pass:
+        // warpgroup `part` owns 16-column chunks c = 16 part + 64 i (i = 0, 1)
+        // of S_base and of S_own (T_pad <= 128), so the S columns are free for
+        // the next head's score MMA as soon as every warp has loaded them.
+        float vb[2][16], vo[2][16];
+        const int cb0 = part * 16, cb1 = part * 16 + 64;
+        const bool lb0 = cb0 < wb_end, lb1 = cb1 < wb_end;
+        const bool lo0 = cb0 >= wo_beg && cb0 < wo_end, lo1 = cb1 >= wo_beg && cb1 < wo_end;
+        if (lb0) tc::tmem_ld16(trow + TS_BASE + cb0, vb[0]);
+        if (lb1) tc::tmem_ld16(trow + TS_BASE + cb1, vb[1]);
+        if (lo0) tc::tmem_ld16(trow + TS_OWN + cb0, vo[0]);
+        if (lo1) tc::tmem_ld16(trow + TS_OWN + cb1, vo[1]);
+        tc::tmem_wait_ld();
         float m = -INFINITY;
-        for (int c0 = part * 16; c0 < wb_end; c0 += 64) {
-          float v[16];
-          tc::tmem_ld16(trow + TS_BASE + c0, v);
-          tc::tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < a) m = fmaxf(m, v[j]);
-        }
-        for (int c0 = wo_beg + part * 16; c0 < wo_end; c0 += 64) {
-          float v[16];
-          tc::tmem_ld16(trow + TS_OWN + c0, v);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j >= own_lo && c0 + j <= own_hi) m = fmaxf(m, v[j]);
+        for (int j = 0; j < 16; ++j) {
+          if (lb0 && cb0 + j < a) m = fmaxf(m, vb[0][j]);
+          if (lb1 && cb1 + j < a) m = fmaxf(m, vb[1][j]);
+          if (lo0 && cb0 + j >= own_lo && cb0 + j <= own_hi) m = fmaxf(m, vo[0][j]);
+          if (lo1 && cb1 + j >= own_lo && cb1 + j <= own_hi) m = fmaxf(m, vo[1][j]);
         }
         red[part][row] = m;
-        __syncthreads();
-        m = fmaxf(fmaxf(red[0][row], red[1][row]), fmaxf(red[2][row], red[3][row])) * sl2;
-        // ---- pass 2: e = exp2(s*scale*log2e - m) on live entries (0 elsewhere), back to TMEM
-        float sum = 0.f;
-        for (int c0 = part * 16; c0 < wb_end; c0 += 64) {
-          float v[16];
-          tc::tmem_ld16(trow + TS_BASE + c0, v);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            v[j] = (c0 + j < a) ? exp2f(fmaf(v[j], sl2, -m)) : 0.f;
-            sum += v[j];
-          }
-          tc::tmem_st16(trow + TS_BASE + c0, v);
-        }
-        for (int c0 = wo_beg + part * 16; c0 < wo_end; c0 += 64) {
-          float v[16];
-          tc::tmem_ld16(trow + TS_OWN + c0, v);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            v[j] = (c0 + j >= own_lo && c0 + j <= own_hi) ? exp2f(fmaf(v[j], sl2, -m)) : 0.f;
-            sum += v[j];
-          }
-          tc::tmem_st16(trow + TS_OWN + c0, v);
-        }
-        tc::tmem_wait_st();
-        red2[part][row] = sum;
         tc::fence_before();
         __syncthreads();
-        tc::fence_after();
+        if (tid == 0 && hh + 1 < hpg) {
+          // S is in registers everywhere: the next head's scores overlap this
+          // head's softmax and value MMA
+          tc::fence_after();
+          issue_scores(hh + 1);
+        }
+        m = fmaxf(fmaxf(red[0][row], red[1][row]), fmaxf(red[2][row], red[3][row])) * sl2;
+        // ---- e = exp2(s*scale*log2e - m) on live entries, 0 elsewhere
+        float sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          vb[0][j] = (lb0 && cb0 + j < a) ? exp2f(fmaf(vb[0][j], sl2, -m)) : 0.f;
+          vb[1][j] = (lb1 && cb1 + j < a) ? exp2f(fmaf(vb[1][j], sl2, -m)) : 0.f;
+          sum += vb[0][j];
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sum += vb[1][j];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          vo[0][j] = (lo0 && cb0 + j >= own_lo && cb0 + j <= own_hi)
+                         ? exp2f(fmaf(vo[0][j], sl2, -m)) : 0.f;
+          vo[1][j] = (lo1 && cb1 + j >= own_lo && cb1 + j <= own_hi)
+                         ? exp2f(fmaf(vo[1][j], sl2, -m)) : 0.f;
+          sum += vo[0][j];
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sum += vo[1][j];
+        red2[part][row] = sum;
+        __syncthreads();
         const float inv = 1.f / (((red2[0][row] + red2[1][row]) + red2[2][row]) + red2[3][row]);
         // P is rewritten only after the previous head's value MMA consumed it
         if (hh > 0) {
           tc::mbar_wait(&mbar[1], ph_o);
           ph_o ^= 1;
         }
-        // ---- pass 3: normalised bf16 probabilities into the P tiles
-        for (int c0 = part * 16; c0 < kb_base; c0 += 64) {
-          uint32_t pk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          if (c0 < wb_end) {
-            float v[16];
-            tc::tmem_ld16(trow + TS_BASE + c0, v);
-            tc::tmem_wait_ld();
+        // ---- normalised bf16 probabilities into the P tiles
+        auto put_p = [&](uint32_t blk0, int c0, const float* v) {
+          uint32_t pk[8];
 #pragma unroll
-            for (int j = 0; j < 16; j += 2) pk[j / 2] = tc::pack_bf16(v[j] * inv, v[j + 1] * inv);
-          }
-          const uint32_t blk = sb + L.pbase + (uint32_t)(c0 >> 6) * (128 * 128);
+          for (int j = 0; j < 16; j += 2) pk[j / 2] = tc::pack_bf16(v[j] * inv, v[j + 1] * inv);
+          const uint32_t blk = blk0 + (uint32_t)(c0 >> 6) * (128 * 128);
           const uint32_t cc = (uint32_t)((c0 & 63) >> 3);
           tc::st_shared_v4(blk + tc::sw128_chunk(row, cc), pk[0], pk[1], pk[2], pk[3]);
           tc::st_shared_v4(blk + tc::sw128_chunk(row, cc + 1), pk[4], pk[5], pk[6], pk[7]);
-        }
-        for (int c0 = part * 16; c0 < 128; c0 += 64) {
-          uint32_t pk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          if (c0 >= wo_beg && c0 < wo_end) {
-            float v[16];
-            tc::tmem_ld16(trow + TS_OWN + c0, v);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 16; j += 2) pk[j / 2] = tc::pack_bf16(v[j] * inv, v[j + 1] * inv);
-          }
-          const uint32_t blk = sb + L.pown + (uint32_t)(c0 >> 6) * (128 * 128);
-          const uint32_t cc = (uint32_t)((c0 & 63) >> 3);
-          tc::st_shared_v4(blk + tc::sw128_chunk(row, cc), pk[0], pk[1], pk[2], pk[3]);
-          tc::st_shared_v4(blk + tc::sw128_chunk(row, cc + 1), pk[4], pk[5], pk[6], pk[7]);
-        }
+        };
+        if (cb0 < kb_base) put_p(sb + L.pbase, cb0, vb[0]);
+        if (cb1 < kb_base) put_p(sb + L.pbase, cb1, vb[1]);
+        put_p(sb + L.pown, cb0, vo[0]);
+        put_p(sb + L.pown, cb1, vo[1]);
         tc::fence_before();
         tc::fence_proxy_async();
         __syncthreads();
         // ---- O_h = P_base V_base + P_own V_own  (V is the MN-major B operand)
         if (tid == 0) {
           tc::fence_after();
-          // the next head's scores first (S was fully read before the barrier
-          // above), so its softmax overlaps this head's value MMA
-          if (hh + 1 < hpg) issue_scores(hh + 1);
           const uint32_t idO = tc::make_idesc_bf16(128, dh) | (1u << 16);
           int first = 1;
           for (int k16 = 0; k16 < kb_base; k16 += 16) {
