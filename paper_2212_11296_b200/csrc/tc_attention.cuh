@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 3);
   // exchange buffers alternate by head: a fast warp may publish head h+1
   // before a slow one has read head h (no block barrier in between)
-  __shared__ float red_m[2][4][128], red_s[2][4][128], nrm[2][4][128];
+  __shared__ float2 red[2][4][128];  // (local max, local sum)
+  __shared__ float nrm[2][4][128];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row = tid & 127, part = tid >> 7;  // warp w owns TMEM lanes 32(w%4)..
   const int KBb = attn_kb_base(T);
@@ -164,7 +165,9 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   const float sl2 = scale * 1.4426950408889634f;
   uint32_t ph_s = 0, ph_o = 0, ph_p = 0, hc = 0;
 
-  auto tile_of = [&](int it) { return tiles[blockIdx.x + (it / G) * gridDim.x]; };
+  // item it = (tile j of this CTA, head group gi), it = j G + gi; counters
+  // advance incrementally (no integer division in the loop)
+  auto tile_of = [&](int j) { return tiles[blockIdx.x + j * gridDim.x]; };
   auto kb_of = [&](int tp) {
     const int m = max(max(wmax[tp * 4 + 0], wmax[tp * 4 + 1]),
                       max(wmax[tp * 4 + 2], wmax[tp * 4 + 3]));
@@ -172,11 +175,11 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   };
   // stage the operands of item `it` (cp.async, zero-filled tails); the first
   // item of a tile first lays out the tile's row table
-  auto prefetch = [&](int it) {
+  auto prefetch = [&](int it, int j, int gi) {
     if (it >= nit) return;
-    const int gi = it % G, tp = (it / G) & 1;
+    const int tp = j & 1;
     if (gi == 0) {
-      const AttnTile tl = tile_of(it);
+      const AttnTile tl = tile_of(j);
       if (part == 0) {
         const int64_t uo = Uoff[tl.sample], base = act_off[tl.sample];
         const bool lv = row < tl.nloc;
@@ -237,8 +240,8 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     tc::mma_commit(&mbar[0]);
   };
 
-  prefetch(0);
-  prefetch(1);
+  prefetch(0, 0, 0);
+  prefetch(1, G == 1 ? 1 : 0, G == 1 ? 0 : 1);
   tc::cp_async_wait<1>();
   tc::fence_proxy_async();
   __syncthreads();
@@ -252,13 +255,16 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   int64_t myloc = 0;
   int kb_base = 0;
   int nb = 0, nq = 0, wo_beg = 0;  // warp's live chunks: nb base + (nq - nb) own from wo_beg
+  int nbf = 0;                     // base chunks every live row of the warp uses entirely
   int a = 0, own_lo = 0, own_cnt = 0;
   float xn2 = 0.f, rr2 = 0.f;
+  int j = 0, gi = 0;  // item it = (j, gi)
   for (int it = 0; it < nit; ++it) {
-    const int gi = it % G, tp = (it / G) & 1;
+    const int tp = j & 1;
+    const int j1 = gi + 1 == G ? j + 1 : j, g1 = gi + 1 == G ? 0 : gi + 1;  // item it + 1
     const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
     if (gi == 0) {
-      const AttnTile tl = tile_of(it);
+      const AttnTile tl = tile_of(j);
       live = row < tl.nloc;
       myloc = tl.loc0 + row;
       a = inf_a[tp * 128 + row];
@@ -271,6 +277,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       wo_beg = w_olo >= 128 ? 128 : (w_olo & ~15);
       const int wo_end = w_ohi < 0 ? 0 : ((w_ohi + 16) & ~15);
       nb = wb_end >> 4;
+      nbf = warp_min_i(live ? a : 1 << 20) >> 4;
       nq = nb + max(0, (wo_end - wo_beg) >> 4);
       xn2 = 0.f;
       rr2 = 0.f;
@@ -309,11 +316,16 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         if (!sl[i]) continue;
+        if (part + 4 * i < nbf) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const bool ok = (unsigned)(off[i] + j) < (unsigned)cnt[i];
-          v[i][j] = ok ? v[i][j] : -INFINITY;
-          mp = fmaxf(mp, v[i][j]);
+          for (int j = 0; j < 16; ++j) mp = fmaxf(mp, v[i][j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const bool ok = (unsigned)(off[i] + j) < (unsigned)cnt[i];
+            v[i][j] = ok ? v[i][j] : -INFINITY;
+            mp = fmaxf(mp, v[i][j]);
+          }
         }
       }
       const float mref = mp == -INFINITY ? 0.f : mp * sl2;
@@ -329,8 +341,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       }
       const int xb = hc & 1;
       ++hc;
-      red_m[xb][part][row] = mp;
-      red_s[xb][part][row] = sp;
+      red[xb][part][row] = make_float2(mp, sp);
       tc::fence_before();
       __syncthreads();
       if (tid == 0 && hh + 1 < hpg) {
@@ -339,16 +350,14 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         tc::fence_after();
         issue_scores(it, hh + 1, kb_base);
       }
-      float m = red_m[xb][0][row];
+      float2 rq[4];
 #pragma unroll
-      for (int q = 1; q < 4; ++q) m = fmaxf(m, red_m[xb][q][row]);
+      for (int q = 0; q < 4; ++q) rq[q] = red[xb][q][row];
+      const float m = fmaxf(fmaxf(rq[0].x, rq[1].x), fmaxf(rq[2].x, rq[3].x));
       float tot = 0.f;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float s_q = red_s[xb][q][row];
-        tot += s_q > 0.f ? s_q * ex2_approx((red_m[xb][q][row] - m) * sl2) : 0.f;
-      }
-      const float f = sp > 0.f ? ex2_approx((mp - m) * sl2) / tot : 0.f;
+      for (int q = 0; q < 4; ++q) tot += rq[q].y > 0.f ? rq[q].y * ex2_approx((rq[q].x - m) * sl2) : 0.f;
+      const float f = sp > 0.f ? __fdividef(ex2_approx((mp - m) * sl2), tot) : 0.f;
       // P is rewritten only after the previous head's value MMA consumed it
       if (hh > 0) {
         tc::mbar_wait(&mbar[1], ph_o);
@@ -399,7 +408,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     __syncthreads();
     if (tid == 0 && it + 1 < nit) {
       tc::fence_after();
-      issue_scores(it + 1, 0, kb_of(((it + 1) / G) & 1));
+      issue_scores(it + 1, 0, kb_of(j1 & 1));
     }
     tc::mbar_wait(&mbar[1], ph_o);  // the item's last value MMA
     ph_o ^= 1;
@@ -441,7 +450,10 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         rr2_out[myloc] = ((nrm[1][0][row] + nrm[1][1][row]) + nrm[1][2][row]) + nrm[1][3][row];
       }
     }
-    prefetch(it + 2);  // into this item's stage: every MMA reading it has completed
+    // into this item's stage: every MMA reading it has completed
+    prefetch(it + 2, g1 + 1 == G ? j1 + 1 : j1, g1 + 1 == G ? 0 : g1 + 1);
+    j = j1;
+    gi = g1;
   }
   tc::fence_before();
   __syncthreads();
