@@ -46,6 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [nvcc(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-O3", "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
+        # developer instrumentation switches (e.g. -DVQNQS_ATTN_TRACE)
+        cmd[1:1] = os.environ.get("VQNQS_EXTRA_NVCC", "").split()
         if src.endswith(".cu"):
             cmd[1:1] = ["--expt-relaxed-constexpr", "-Xptxas", "-v"] if verbose else \
                 ["--expt-relaxed-constexpr"]

@@ -157,6 +157,7 @@ class EngineImpl {
   DBuf<char> h_, qkv_, f1_;
   DBuf<uint8_t> cfg_stage_;
   DBuf<AttnTile> tiles_;
+  DBuf<uint8_t> tinfo_;
   DBuf<int32_t> ntiles_;
   DBuf<double> out_stage_;
   DBuf<int32_t> taps_codes_;
@@ -487,6 +488,13 @@ class EngineImpl {
                                                          act_off_.p, tiles_.p, ntiles_.p);
           ++launches;
         }
+        // per-layer tile tables (qkv rows follow this layer's dedup); at most
+        // 2 M / 128 + 3 S tiles (two consecutive tiles of a sample hold > 128)
+        const int64_t tcap = std::min<int64_t>(R, M / 64 + 3 * int64_t(S) + 16);
+        tinfo_.ensure(size_t(tcap) * TINFO_BYTES);
+        k_tile_info<<<sms * 8, 128, 0, st>>>(tiles_.p, ntiles_.p, R1, T, row_t1_.p, act_off_.p,
+                                             lrow_.p, lpos_.p, Icur, Uo_cur, tinfo_.p);
+        ++launches;
         const size_t asmem = AttnSmem(T).total + 1024;
         static size_t attr = 0;
         if (attr < asmem) {
@@ -495,8 +503,8 @@ class EngineImpl {
           attr = asmem;
         }
         k_tc_attention<<<sms, TCA_THREADS, asmem, st>>>(
-            tiles_.p, ntiles_.p, R1, T, d, dh, scale, row_t1_.p, act_off_.p, lrow_.p, lpos_.p,
-            Icur, Uo_cur, reinterpret_cast<const bf16*>(qkv), att_hi_.p, att_lo_.p, xn2_.p, rr2_.p);
+            tinfo_.p, ntiles_.p, T, d, dh, scale, reinterpret_cast<const bf16*>(qkv), att_hi_.p,
+            att_lo_.p, xn2_.p, rr2_.p);
       } else {
         const size_t asmem = (size_t(T) * (dh + 1) + size_t(T) * dh + 4 * T + 4 * dh) * 4;
         if (asmem > 48 * 1024)

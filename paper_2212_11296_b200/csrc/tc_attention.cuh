@@ -81,11 +81,66 @@ __global__ void k_build_tiles(int S, int R1, int T, const int32_t* __restrict__ 
 __host__ __device__ inline int attn_tpad(int T) { return ((T + 15) / 16) * 16; }
 __host__ __device__ inline int attn_kb_base(int T) { return (attn_tpad(T) + 63) / 64; }
 
+__device__ __forceinline__ int warp_max_i(int v) { return __reduce_max_sync(0xffffffffu, v); }
+__device__ __forceinline__ int warp_min_i(int v) { return __reduce_min_sync(0xffffffffu, v); }
+
+// Per-tile row table, rebuilt per layer (the qkv row of a location depends on
+// the layer's dedup). 1552 bytes per tile, fetched by the attention kernel
+// with plain 16-byte async copies one tile ahead:
+//   [0, 512)     int32 qkv row of tile row r (-1 past the tile)
+//   [512, 1024)  int32 qkv row of base-row position t (-1 for t >= T)
+//   [1024, 1280) int16 a_r: base keys of row r
+//   [1280, 1536) int16 own_lo_r: first own key (tile row) of row r
+//   [1536, 1552) int64 loc0, int32 nloc, int32 kb_base (16 ceil(max a))
+constexpr int TINFO_BYTES = 1552;
+
+__global__ void __launch_bounds__(128) k_tile_info(
+    const AttnTile* __restrict__ tiles, const int32_t* __restrict__ n_tiles_p, int R1, int T,
+    const int32_t* __restrict__ row_t1, const int64_t* __restrict__ act_off,
+    const int32_t* __restrict__ lrow, const int16_t* __restrict__ lpos,
+    const int32_t* __restrict__ I, const int64_t* __restrict__ Uoff,
+    uint8_t* __restrict__ tinfo) {
+  __shared__ int wm[4];
+  const int n_tiles = *n_tiles_p;
+  const int r = threadIdx.x;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const AttnTile tl = tiles[t];
+    uint8_t* blk = tinfo + (int64_t)t * TINFO_BYTES;
+    const int64_t uo = Uoff[tl.sample], base = act_off[tl.sample];
+    const bool lv = r < tl.nloc;
+    int a = 0, lo = 0x7fff;
+    if (lv) {
+      const int64_t loc = tl.loc0 + r;
+      const int rr = lrow[loc];
+      const int p = lpos[loc];
+      a = (rr % R1) == 0 ? 0 : row_t1[rr] + 1;
+      lo = r - (p - a);
+    }
+    reinterpret_cast<int32_t*>(blk)[r] = lv ? (int32_t)(uo + I[tl.loc0 + r]) : -1;
+    reinterpret_cast<int32_t*>(blk + 512)[r] = r < T ? (int32_t)(uo + I[base + r]) : -1;
+    reinterpret_cast<int16_t*>(blk + 1024)[r] = (int16_t)a;
+    reinterpret_cast<int16_t*>(blk + 1280)[r] = (int16_t)lo;
+    const int m = warp_max_i(a);
+    if ((r & 31) == 0) wm[r >> 5] = m;
+    __syncthreads();
+    if (r == 0) {
+      *reinterpret_cast<int64_t*>(blk + 1536) = tl.loc0;
+      reinterpret_cast<int32_t*>(blk + 1544)[0] = tl.nloc;
+      reinterpret_cast<int32_t*>(blk + 1544)[1] =
+          (max(max(wm[0], wm[1]), max(wm[2], wm[3])) + 15) & ~15;
+    }
+    __syncthreads();
+  }
+}
+
 // shared memory carve (bytes; stages 1024-aligned). Two staging buffers, each
 // q | k_own | v_own (128 x 64) | k_base | v_base (64 KBb x 64), so the operands
-// of the next (tile, head group) item load while the current one computes.
+// of the next (tile, head group) item load while the current one computes;
+// four tile-table slots (fetched one tile ahead); the O staging tile for
+// coalesced stores (xh | xl, 128 rows x 144 B: conflict-free 16-B writes).
+constexpr int ATT_OPITCH = 144;
 struct AttnSmem {
-  uint32_t stage, q, kown, vown, kbase, vbase, rows, info, bar, total;
+  uint32_t stage, q, kown, vown, kbase, vbase, info, out, bar, total;
   __host__ __device__ AttnSmem(int T) {
     const uint32_t KBb = (uint32_t)attn_kb_base(T);
     q = 0;
@@ -94,15 +149,20 @@ struct AttnSmem {
     kbase = 3 * 128 * 128;
     vbase = kbase + 64 * KBb * 128;
     stage = vbase + 64 * KBb * 128;
-    rows = 2 * stage;    // int64 rowq[2][128], rowb[2][128]
-    info = rows + 4096;  // int32 a[2][128], own_lo[2][128], wmax[2][4]
-    bar = info + 2048 + 32;
-    total = bar + 64;
+    info = 2 * stage;
+    out = info + 4 * TINFO_BYTES;
+    bar = out + 2 * 128 * ATT_OPITCH;
+    total = bar + 64;  // 2 mbarriers, TMEM base, P counter
   }
 };
 
-__device__ __forceinline__ int warp_max_i(int v) { return __reduce_max_sync(0xffffffffu, v); }
-__device__ __forceinline__ int warp_min_i(int v) { return __reduce_min_sync(0xffffffffu, v); }
+#ifdef VQNQS_ATTN_TRACE
+#define ATR_DECL unsigned long long atr[16] = {0}; long long atr_t = clock64();
+#define ATR(k) { const long long _n = clock64(); atr[k] += _n - atr_t; atr_t = _n; }
+#else
+#define ATR_DECL
+#define ATR(k)
+#endif
 
 constexpr int TCA_THREADS = 512;
 
@@ -113,23 +173,17 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
-    const AttnTile* __restrict__ tiles, const int32_t* __restrict__ n_tiles_p, int R1, int T,
-    int d, int dh, float scale, const int32_t* __restrict__ row_t1,
-    const int64_t* __restrict__ act_off, const int32_t* __restrict__ lrow,
-    const int16_t* __restrict__ lpos, const int32_t* __restrict__ I,
-    const int64_t* __restrict__ Uoff, const bf16* __restrict__ qkv, bf16* __restrict__ xh_out,
+    const uint8_t* __restrict__ tinfo, const int32_t* __restrict__ n_tiles_p, int T, int d,
+    int dh, float scale, const bf16* __restrict__ qkv, bf16* __restrict__ xh_out,
     bf16* __restrict__ xl_out, float* __restrict__ xn2_out, float* __restrict__ rr2_out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const AttnSmem L(T);
-  int64_t* rowq = reinterpret_cast<int64_t*>(smem + L.rows);  // [2][128] qkv offsets, tile rows
-  int64_t* rowb = rowq + 256;                                 // [2][128] ... base rows
-  int32_t* inf_a = reinterpret_cast<int32_t*>(smem + L.info);  // [2][128]
-  int32_t* inf_lo = inf_a + 256;                               // [2][128]
-  int32_t* wmax = inf_lo + 256;                                // [2][4]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.bar);  // S full, PV done, P ready
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 3);
+  const uint8_t* info = smem + L.info;  // 4 tile-table slots (k_tile_info layout)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.bar);  // [0] S ready, [1] PV done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+  uint32_t* p_cnt = tmem_slot + 1;  // warps done writing P (16 per head)
   // exchange buffers alternate by head: a fast warp may publish head h+1
   // before a slow one has read head h (no block barrier in between)
   __shared__ float2 red[2][4][128];  // (local max, local sum)
@@ -141,7 +195,6 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   const int TP = attn_tpad(T);
   const int G = d / 64;
   const int hpg = 64 / dh;  // heads per 64-wide group
-  const int ld = 3 * d;
   const int my_tiles =
       (int)blockIdx.x < n_tiles ? (n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
                                 : 0;
@@ -149,7 +202,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   if (tid == 0) {
     tc::mbar_init(&mbar[0], 1);
     tc::mbar_init(&mbar[1], 1);
-    tc::mbar_init(&mbar[2], TCA_THREADS / 32);
+    *p_cnt = 0;
     tc::mbar_fence_init();
   }
   if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
@@ -163,49 +216,33 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
                  TS_O = TS_P + (uint32_t)(TP + 128) / 2;
   const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const float sl2 = scale * 1.4426950408889634f;
-  uint32_t ph_s = 0, ph_o = 0, ph_p = 0, hc = 0;
+  const int ld = 3 * d;
+  uint32_t ph_s = 0, ph_o = 0, hc = 0;
+  ATR_DECL
 
   // item it = (tile j of this CTA, head group gi), it = j G + gi; counters
   // advance incrementally (no integer division in the loop)
-  auto tile_of = [&](int j) { return tiles[blockIdx.x + j * gridDim.x]; };
-  auto kb_of = [&](int tp) {
-    const int m = max(max(wmax[tp * 4 + 0], wmax[tp * 4 + 1]),
-                      max(wmax[tp * 4 + 2], wmax[tp * 4 + 3]));
-    return (m + 15) & ~15;  // base keys any row of the tile uses
+  auto slot = [&](int j) { return info + (j & 3) * TINFO_BYTES; };
+  auto kb_of = [&](int j) { return reinterpret_cast<const int32_t*>(slot(j) + 1548)[0]; };
+  // async copy of tile j's table into its slot (part of the caller's group)
+  auto fetch_info = [&](int j) {
+    if (j < my_tiles && tid < TINFO_BYTES / 16) {
+      const uint8_t* src = tinfo + (int64_t)(blockIdx.x + j * gridDim.x) * TINFO_BYTES;
+      tc::cp_async16(sb + L.info + (uint32_t)((j & 3) * TINFO_BYTES) + tid * 16, src + tid * 16);
+    }
   };
-  // stage the operands of item `it` (cp.async, zero-filled tails); the first
-  // item of a tile first lays out the tile's row table
+  // stage the operands of item `it` = (j, gi) (cp.async, zero-filled tails);
+  // the first item of tile j >= 1 also fetches tile j+1's table (tables 0
+  // and 1 are fetched up front)
   auto prefetch = [&](int it, int j, int gi) {
     if (it >= nit) return;
-    const int tp = j & 1;
-    if (gi == 0) {
-      const AttnTile tl = tile_of(j);
-      if (part == 0) {
-        const int64_t uo = Uoff[tl.sample], base = act_off[tl.sample];
-        const bool lv = row < tl.nloc;
-        int a = 0, lo = 1 << 20;
-        if (lv) {
-          const int64_t loc = tl.loc0 + row;
-          const int r = lrow[loc];
-          const int p = lpos[loc];
-          a = (r % R1) == 0 ? 0 : row_t1[r] + 1;
-          lo = row - (p - a);
-        }
-        rowq[tp * 128 + row] = lv ? (uo + I[tl.loc0 + row]) * ld : -1;
-        rowb[tp * 128 + row] = row < T ? (uo + I[base + row]) * ld : -1;
-        inf_a[tp * 128 + row] = a;
-        inf_lo[tp * 128 + row] = lo;
-        const int wm = warp_max_i(a);
-        if (lane == 0) wmax[tp * 4 + warp] = wm;
-      }
-      __syncthreads();
-    }
+    if (gi == 0 && j >= 1) fetch_info(j + 1);
     const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
-    const int64_t* rq = rowq + tp * 128;
-    const int64_t* rb = rowb + tp * 128;
+    const int32_t* rq = reinterpret_cast<const int32_t*>(slot(j));
+    const int32_t* rb = rq + 128;
     for (int e = tid; e < 128 * 8; e += TCA_THREADS) {
       const int r = e >> 3, c = e & 7;
-      const int64_t off = rq[r];
+      const int64_t off = (int64_t)rq[r] * ld;
       const bool ok = off >= 0;
       const bf16* src = qkv + (ok ? off : 0) + gi * 64 + c * 8;
       const uint32_t o = tc::sw128_chunk(r, c);
@@ -215,7 +252,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     }
     for (int e = tid; e < 64 * KBb * 8; e += TCA_THREADS) {
       const int t = e >> 3, c = e & 7;
-      const int64_t off = t < 128 ? rb[t] : -1;
+      const int64_t off = t < 128 ? (int64_t)rb[t] * ld : -1;
       const bool ok = off >= 0;
       const bf16* src = qkv + (ok ? off : 0) + d + gi * 64 + c * 8;
       const uint32_t o = tc::sw128_chunk(t, c);
@@ -230,16 +267,22 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     const uint32_t qoff = (uint32_t)(hq * dh * 2);  // head offset inside the 128-B row
     const uint32_t idS_b = tc::make_idesc_bf16(128, kb_base > 0 ? kb_base : 16);
     const uint32_t idS_o = tc::make_idesc_bf16(128, 128);
-    for (int k = 0; k < dh / 16; ++k) {
+    const uint64_t dq = tc::make_desc_sw128(st + L.q + qoff);
+    const uint64_t dkb = tc::make_desc_sw128(st + L.kbase + qoff);
+    const uint64_t dko = tc::make_desc_sw128(st + L.kown + qoff);
+    for (int k = 0; k < dh / 16; ++k) {  // +32 B along K = +2 in the descriptor
       if (kb_base > 0)
-        tc::mma_bf16(tmem + TS_BASE, tc::make_desc_sw128(st + L.q + qoff + k * 32),
-                     tc::make_desc_sw128(st + L.kbase + qoff + k * 32), idS_b, k != 0);
-      tc::mma_bf16(tmem + TS_OWN, tc::make_desc_sw128(st + L.q + qoff + k * 32),
-                   tc::make_desc_sw128(st + L.kown + qoff + k * 32), idS_o, k != 0);
+        tc::mma_bf16(tmem + TS_BASE, dq + 2 * k, dkb + 2 * k, idS_b, k != 0);
+      tc::mma_bf16(tmem + TS_OWN, dq + 2 * k, dko + 2 * k, idS_o, k != 0);
     }
     tc::mma_commit(&mbar[0]);
   };
 
+  fetch_info(0);
+  fetch_info(1);
+  tc::cp_async_commit();
+  tc::cp_async_wait<0>();
+  __syncthreads();
   prefetch(0, 0, 0);
   prefetch(1, G == 1 ? 1 : 0, G == 1 ? 0 : 1);
   tc::cp_async_wait<1>();
@@ -255,29 +298,28 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   int64_t myloc = 0;
   int kb_base = 0;
   int nb = 0, nq = 0, wo_beg = 0;  // warp's live chunks: nb base + (nq - nb) own from wo_beg
-  int nbf = 0;                     // base chunks every live row of the warp uses entirely
   int a = 0, own_lo = 0, own_cnt = 0;
   float xn2 = 0.f, rr2 = 0.f;
+  int nloc = 0;
   int j = 0, gi = 0;  // item it = (j, gi)
   for (int it = 0; it < nit; ++it) {
-    const int tp = j & 1;
     const int j1 = gi + 1 == G ? j + 1 : j, g1 = gi + 1 == G ? 0 : gi + 1;  // item it + 1
     const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
     if (gi == 0) {
-      const AttnTile tl = tile_of(j);
-      live = row < tl.nloc;
-      myloc = tl.loc0 + row;
-      a = inf_a[tp * 128 + row];
-      own_lo = inf_lo[tp * 128 + row];
+      const uint8_t* ti = slot(j);
+      nloc = reinterpret_cast<const int32_t*>(ti + 1544)[0];
+      live = row < nloc;
+      myloc = *reinterpret_cast<const int64_t*>(ti + 1536) + row;
+      a = reinterpret_cast<const int16_t*>(ti + 1024)[row];
+      own_lo = reinterpret_cast<const int16_t*>(ti + 1280)[row];
       own_cnt = live ? row - own_lo + 1 : 0;
-      kb_base = kb_of(tp);
+      kb_base = kb_of(j);
       const int wb_end = (warp_max_i(a) + 15) & ~15;
       const int w_olo = warp_min_i(live ? own_lo : 1 << 20);
       const int w_ohi = warp_max_i(live ? row : -1);
       wo_beg = w_olo >= 128 ? 128 : (w_olo & ~15);
       const int wo_end = w_ohi < 0 ? 0 : ((w_ohi + 16) & ~15);
       nb = wb_end >> 4;
-      nbf = warp_min_i(live ? a : 1 << 20) >> 4;
       nq = nb + max(0, (wo_end - wo_beg) >> 4);
       xn2 = 0.f;
       rr2 = 0.f;
@@ -287,16 +329,18 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       for (int c = part * 8; c < pcols; c += 32) tc::tmem_st8u(trow + TS_P + c, zero);
       tc::tmem_wait_st();
     }
+    ATR(12)
     for (int hh = 0; hh < hpg; ++hh) {
       const uint32_t koff = (uint32_t)(hh * dh * 2);  // head offset inside the 128-B row
       tc::mbar_wait(&mbar[0], ph_s);
       ph_s ^= 1;
       tc::fence_after();
+      ATR(0)
       // ---- the warp's live 16-column chunks (base chunks, then own chunks)
       // are dealt round-robin to the four warpgroups: slot i is chunk part + 4i.
       // ONE TMEM pass loads them into registers.
       float v[4][16];
-      bool sl[4];
+      bool sl[4], full[4];
       int off[4], cnt[4];
       uint32_t pcol[4];
 #pragma unroll
@@ -308,23 +352,26 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         off[i] = isb ? c0 : c0 - own_lo;  // entry j is live iff 0 <= off + j < cnt
         cnt[i] = isb ? a : own_cnt;
         pcol[i] = (uint32_t)((isb ? c0 : kb_base + c0) >> 1);
+        // chunk live in full for every live row of the warp: no masking
+        full[i] = __all_sync(0xffffffffu, !live || (off[i] >= 0 && off[i] + 16 <= cnt[i]));
         if (sl[i]) tc::tmem_ld16(trow + (isb ? TS_BASE : TS_OWN) + c0, v[i]);
       }
       tc::tmem_wait_ld();
+      ATR(1)
       // ---- local max and sum of exp2((s - m_part) * scale * log2e)
       float mp = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         if (!sl[i]) continue;
-        if (part + 4 * i < nbf) {
+        if (full[i]) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) mp = fmaxf(mp, v[i][j]);
+          for (int q = 0; q < 16; ++q) mp = fmaxf(mp, v[i][q]);
         } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const bool ok = (unsigned)(off[i] + j) < (unsigned)cnt[i];
-            v[i][j] = ok ? v[i][j] : -INFINITY;
-            mp = fmaxf(mp, v[i][j]);
+          for (int q = 0; q < 16; ++q) {
+            const bool ok = (unsigned)(off[i] + q) < (unsigned)cnt[i];
+            v[i][q] = ok ? v[i][q] : -INFINITY;
+            mp = fmaxf(mp, v[i][q]);
           }
         }
       }
@@ -334,16 +381,18 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       for (int i = 0; i < 4; ++i) {
         if (!sl[i]) continue;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          v[i][j] = ex2_approx(fmaf(v[i][j], sl2, -mref));
-          sp += v[i][j];
+        for (int q = 0; q < 16; ++q) {
+          v[i][q] = ex2_approx(fmaf(v[i][q], sl2, -mref));
+          sp += v[i][q];
         }
       }
       const int xb = hc & 1;
       ++hc;
       red[xb][part][row] = make_float2(mp, sp);
+      ATR(2)
       tc::fence_before();
       __syncthreads();
+      ATR(3)
       if (tid == 0 && hh + 1 < hpg) {
         // every warp holds its scores in registers: the next head's score
         // MMA overlaps this head's softmax and value MMA
@@ -356,47 +405,53 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       const float m = fmaxf(fmaxf(rq[0].x, rq[1].x), fmaxf(rq[2].x, rq[3].x));
       float tot = 0.f;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tot += rq[q].y > 0.f ? rq[q].y * ex2_approx((rq[q].x - m) * sl2) : 0.f;
+      for (int q = 0; q < 4; ++q)
+        tot += rq[q].y > 0.f ? rq[q].y * ex2_approx((rq[q].x - m) * sl2) : 0.f;
       const float f = sp > 0.f ? __fdividef(ex2_approx((mp - m) * sl2), tot) : 0.f;
       // P is rewritten only after the previous head's value MMA consumed it
+      ATR(4)
       if (hh > 0) {
         tc::mbar_wait(&mbar[1], ph_o);
         ph_o ^= 1;
       }
+      ATR(5)
       // ---- normalised bf16 probabilities into the TMEM P tile
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         if (!sl[i]) continue;
         uint32_t pk[8];
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) pk[j / 2] = tc::pack_bf16(v[i][j] * f, v[i][j + 1] * f);
+        for (int q = 0; q < 16; q += 2) pk[q / 2] = tc::pack_bf16(v[i][q] * f, v[i][q + 1] * f);
         tc::tmem_st8u(trow + TS_P + pcol[i], pk);
       }
       tc::tmem_wait_st();
+      ATR(6)
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&mbar[2]));
-      // ---- O_h = P_base V_base + P_own V_own  (P from TMEM, V the MN-major B operand)
-      if (tid == 0) {
-        tc::mbar_wait(&mbar[2], ph_p);
-        tc::fence_after();
-        const uint32_t idO = tc::make_idesc_bf16(128, dh) | (1u << 16);
-        int first = 1;
-        for (int k16 = 0; k16 < kb_base; k16 += 16) {
-          tc::mma_bf16_ts(tmem + TS_O + hh * dh, tmem + TS_P + (uint32_t)(k16 >> 1),
-                          tc::make_desc_sw128(st + L.vbase + (uint32_t)k16 * 128 + koff), idO,
-                          first ? 0u : 1u);
-          first = 0;
+      // ---- O_h = P_base V_base + P_own V_own (P from TMEM, V the MN-major B
+      // operand), issued by the LAST warp to finish its P columns, so no warp
+      // idles waiting for the others
+      if (lane == 0) {
+        __threadfence_block();
+        if ((atomicAdd(p_cnt, 1u) & 15u) == 15u) {
+          __threadfence_block();
+          tc::fence_after();
+          const uint32_t idO = tc::make_idesc_bf16(128, dh) | (1u << 16);
+          const uint32_t tO = tmem + TS_O + hh * dh, tA = tmem + TS_P;
+          const uint64_t db = tc::make_desc_sw128(st + L.vbase + koff);
+          const uint64_t dw = tc::make_desc_sw128(st + L.vown + koff);
+          // descriptor start field is address >> 4: 16 key rows = +128
+          for (int k16 = 0; k16 < kb_base; k16 += 16)
+            tc::mma_bf16_ts(tO, tA + (uint32_t)(k16 >> 1), db + (uint64_t)(k16 * 8), idO,
+                            k16 > 0 ? 1u : 0u);
+          for (int k16 = 0; k16 < 128; k16 += 16)
+            tc::mma_bf16_ts(tO, tA + (uint32_t)((kb_base + k16) >> 1), dw + (uint64_t)(k16 * 8),
+                            idO, (kb_base > 0 || k16 > 0) ? 1u : 0u);
+          tc::mma_commit(&mbar[1]);
         }
-        for (int k16 = 0; k16 < 128; k16 += 16) {
-          tc::mma_bf16_ts(tmem + TS_O + hh * dh, tmem + TS_P + (uint32_t)((kb_base + k16) >> 1),
-                          tc::make_desc_sw128(st + L.vown + (uint32_t)k16 * 128 + koff), idO,
-                          first ? 0u : 1u);
-          first = 0;
-        }
-        tc::mma_commit(&mbar[1]);
       }
-      ph_p ^= 1;
+      __syncwarp();
+      ATR(7)
     }
     // ---- next item's operands landed -> its first score MMA runs while this
     // item's O drains
@@ -408,38 +463,60 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     __syncthreads();
     if (tid == 0 && it + 1 < nit) {
       tc::fence_after();
-      issue_scores(it + 1, 0, kb_of(j1 & 1));
+      issue_scores(it + 1, 0, kb_of(j1));
     }
+    ATR(8)
     tc::mbar_wait(&mbar[1], ph_o);  // the item's last value MMA
     ph_o ^= 1;
     tc::fence_after();
-    // ---- drain O: warpgroup `part` takes columns [16 part, 16 part + 16)
+    ATR(9)
+    // ---- drain O: warpgroup `part` takes columns [16 part, 16 part + 16) of
+    // its rows into the staging tile; the quadrant's four warps then store
+    // whole 128-B row segments
     {
       float o[16];
       tc::tmem_ld16(trow + TS_O + part * 16, o);  // warp-collective: every lane loads
       tc::tmem_wait_ld();
-      if (live) {
-        uint32_t ph[8], pl[8];
+      uint32_t ph[8], pl[8];
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-          ph[j / 2] = tc::pack_bf16(o[j], o[j + 1]);
-          const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&ph[j / 2]);
-          const float d0 = o[j] - __low2float(h), d1 = o[j + 1] - __high2float(h);
-          pl[j / 2] = tc::pack_bf16(d0, d1);
-          const __nv_bfloat162 l = *reinterpret_cast<const __nv_bfloat162*>(&pl[j / 2]);
-          const float r0 = __low2float(l), r1 = __high2float(l);  // |xl|^2 (tc_vq.cuh)
-          xn2 = fmaf(o[j], o[j], fmaf(o[j + 1], o[j + 1], xn2));
-          rr2 = fmaf(r0, r0, fmaf(r1, r1, rr2));
+      for (int q = 0; q < 16; q += 2) {
+        ph[q / 2] = tc::pack_bf16(o[q], o[q + 1]);
+        const float h0 = __uint_as_float(ph[q / 2] << 16);
+        const float h1 = __uint_as_float(ph[q / 2] & 0xffff0000u);
+        pl[q / 2] = tc::pack_bf16(o[q] - h0, o[q + 1] - h1);
+        const float r0 = __uint_as_float(pl[q / 2] << 16);
+        const float r1 = __uint_as_float(pl[q / 2] & 0xffff0000u);  // |xl|^2 (tc_vq.cuh)
+        xn2 = fmaf(o[q], o[q], fmaf(o[q + 1], o[q + 1], xn2));
+        rr2 = fmaf(r0, r0, fmaf(r1, r1, rr2));
+      }
+      const uint32_t ob = sb + L.out + (uint32_t)(row * ATT_OPITCH + part * 32);
+      tc::st_shared_v4(ob, ph[0], ph[1], ph[2], ph[3]);
+      tc::st_shared_v4(ob + 16, ph[4], ph[5], ph[6], ph[7]);
+      tc::st_shared_v4(ob + 128 * ATT_OPITCH, pl[0], pl[1], pl[2], pl[3]);
+      tc::st_shared_v4(ob + 128 * ATT_OPITCH + 16, pl[4], pl[5], pl[6], pl[7]);
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + (warp & 3)) : "memory");
+      // quadrant rows 32 q .. 32 q + 31, xh then xl: 64 segments of 128 B,
+      // 8 lanes per segment, 4 segments per warp instruction
+      const int q0 = (warp & 3) * 32;
+      const int64_t loc0 = myloc - row;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int seg = (part * 4 + k) * 4 + (lane >> 3);  // 0..63
+        const int rr = q0 + (seg & 31);
+        if (rr < nloc) {
+          const uint32_t src =
+              sb + L.out + (uint32_t)((seg >> 5) * 128 * ATT_OPITCH + rr * ATT_OPITCH +
+                                      (lane & 7) * 16);
+          uint32_t w0, w1, w2, w3;
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                       : "r"(src));
+          bf16* dst = ((seg >> 5) ? xl_out : xh_out) + (loc0 + rr) * d + gi * 64 + (lane & 7) * 8;
+          *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
         }
-        uint4* oh = reinterpret_cast<uint4*>(xh_out + myloc * d + gi * 64 + part * 16);
-        uint4* ol = reinterpret_cast<uint4*>(xl_out + myloc * d + gi * 64 + part * 16);
-        oh[0] = make_uint4(ph[0], ph[1], ph[2], ph[3]);
-        oh[1] = make_uint4(ph[4], ph[5], ph[6], ph[7]);
-        ol[0] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
-        ol[1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
       }
     }
-    tc::fence_before();
+    ATR(10)
     if (gi == G - 1) {
       // row norms |x|^2 and |x - xh - xl|^2, reduced over the four warpgroups
       nrm[0][part][row] = xn2;
@@ -452,9 +529,16 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     }
     // into this item's stage: every MMA reading it has completed
     prefetch(it + 2, g1 + 1 == G ? j1 + 1 : j1, g1 + 1 == G ? 0 : g1 + 1);
+    ATR(11)
     j = j1;
     gi = g1;
   }
+#ifdef VQNQS_ATTN_TRACE
+  if (blockIdx.x < 2 && lane == 0 && (warp == 0 || warp == 5 || warp == 10 || warp == 15))
+    printf("ATR b%d w%2d items %d: wS %llu ld %llu sm %llu bar %llu comb %llu wPV %llu P %llu arr %llu | end %llu wPVl %llu drain %llu nrm+pf %llu setup %llu\n",
+           blockIdx.x, warp, nit, atr[0], atr[1], atr[2], atr[3], atr[4], atr[5], atr[6], atr[7],
+           atr[8], atr[9], atr[10], atr[11], atr[12]);
+#endif
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem, 512);
