@@ -152,7 +152,7 @@ struct AttnSmem {
     info = 2 * stage;
     out = info + 4 * TINFO_BYTES;
     bar = out + 2 * 128 * ATT_OPITCH;
-    total = bar + 64;  // 2 mbarriers, TMEM base, P counter
+    total = bar + 64;  // 6 mbarriers, TMEM base
   }
 };
 
@@ -164,13 +164,26 @@ struct AttnSmem {
 #define ATR(k)
 #endif
 
-constexpr int TCA_THREADS = 512;
-
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// 16 softmax warps (warp w: TMEM lanes 32(w%4).., column slots of warpgroup
+// w/4) + one MMA warp. All hand-offs are mbarriers or quadrant-local named
+// barriers (the four warps that share a row quadrant), so no block barrier
+// runs per head or per item:
+//   s_full   (MMA commit)      S(g) in TMEM
+//   s_free   (16 warp arrivals) every warp holds S(g) in registers
+//   p_full   (16 warp arrivals) P(g) written to TMEM
+//   pv_done  (MMA commit)      O += P(g) V done, P free
+//   st_full[2] (16 warp arrivals) the item's cp.async operands landed
+// The MMA warp sits in a fifth warpgroup that hands its registers to the
+// softmax warpgroups (setmaxnreg within the launch allocation 640 x 96:
+// 4 x 128 x 112 + 128 x 32).
+constexpr int TCA_SOFTMAX_WARPS = 16;
+constexpr int TCA_THREADS = 32 * (TCA_SOFTMAX_WARPS + 4);
 
 __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     const uint8_t* __restrict__ tinfo, const int32_t* __restrict__ n_tiles_p, int T, int d,
@@ -181,28 +194,36 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
                                              ~uintptr_t(1023));
   const AttnSmem L(T);
   const uint8_t* info = smem + L.info;  // 4 tile-table slots (k_tile_info layout)
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.bar);  // [0] S ready, [1] PV done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
-  uint32_t* p_cnt = tmem_slot + 1;  // warps done writing P (16 per head)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  uint64_t* s_full = mbar + 0;
+  uint64_t* s_free = mbar + 1;
+  uint64_t* p_full = mbar + 2;
+  uint64_t* pv_done = mbar + 3;
+  uint64_t* st_full = mbar + 4;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 6);
   // exchange buffers alternate by head: a fast warp may publish head h+1
-  // before a slow one has read head h (no block barrier in between)
+  // before a slow one of its quadrant has read head h
   __shared__ float2 red[2][4][128];  // (local max, local sum)
   __shared__ float nrm[2][4][128];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int row = tid & 127, part = tid >> 7;  // warp w owns TMEM lanes 32(w%4)..
+  const int row = tid & 127, part = (tid >> 7) & 3;  // warp w owns TMEM lanes 32(w%4)..
   const int KBb = attn_kb_base(T);
   const int n_tiles = *n_tiles_p;
   const int TP = attn_tpad(T);
   const int G = d / 64;
   const int hpg = 64 / dh;  // heads per 64-wide group
+  const int ld = 3 * d;
   const int my_tiles =
       (int)blockIdx.x < n_tiles ? (n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
                                 : 0;
   const int nit = my_tiles * G;  // work items: (tile, head group)
   if (tid == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
-    *p_cnt = 0;
+    tc::mbar_init(s_full, 1);
+    tc::mbar_init(s_free, TCA_SOFTMAX_WARPS);
+    tc::mbar_init(p_full, TCA_SOFTMAX_WARPS);
+    tc::mbar_init(pv_done, 1);
+    tc::mbar_init(&st_full[0], TCA_SOFTMAX_WARPS);
+    tc::mbar_init(&st_full[1], TCA_SOFTMAX_WARPS);
     tc::mbar_fence_init();
   }
   if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
@@ -214,331 +235,364 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   // TMEM columns: S_base | S_own | P (bf16 pairs) | O(group)
   const uint32_t TS_BASE = 0, TS_OWN = (uint32_t)TP, TS_P = (uint32_t)TP + 128,
                  TS_O = TS_P + (uint32_t)(TP + 128) / 2;
-  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-  const float sl2 = scale * 1.4426950408889634f;
-  const int ld = 3 * d;
-  uint32_t ph_s = 0, ph_o = 0, hc = 0;
-  ATR_DECL
-
-  // item it = (tile j of this CTA, head group gi), it = j G + gi; counters
-  // advance incrementally (no integer division in the loop)
   auto slot = [&](int j) { return info + (j & 3) * TINFO_BYTES; };
   auto kb_of = [&](int j) { return reinterpret_cast<const int32_t*>(slot(j) + 1548)[0]; };
-  // async copy of tile j's table into its slot (part of the caller's group)
-  auto fetch_info = [&](int j) {
-    if (j < my_tiles && tid < TINFO_BYTES / 16) {
-      const uint8_t* src = tinfo + (int64_t)(blockIdx.x + j * gridDim.x) * TINFO_BYTES;
-      tc::cp_async16(sb + L.info + (uint32_t)((j & 3) * TINFO_BYTES) + tid * 16, src + tid * 16);
-    }
-  };
-  // stage the operands of item `it` = (j, gi) (cp.async, zero-filled tails);
-  // the first item of tile j >= 1 also fetches tile j+1's table (tables 0
-  // and 1 are fetched up front)
-  auto prefetch = [&](int it, int j, int gi) {
-    if (it >= nit) return;
-    if (gi == 0 && j >= 1) fetch_info(j + 1);
-    const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
-    const int32_t* rq = reinterpret_cast<const int32_t*>(slot(j));
-    const int32_t* rb = rq + 128;
-    for (int e = tid; e < 128 * 8; e += TCA_THREADS) {
-      const int r = e >> 3, c = e & 7;
-      const int64_t off = (int64_t)rq[r] * ld;
-      const bool ok = off >= 0;
-      const bf16* src = qkv + (ok ? off : 0) + gi * 64 + c * 8;
-      const uint32_t o = tc::sw128_chunk(r, c);
-      tc::cp_async16_zfill(st + L.q + o, src, ok);
-      tc::cp_async16_zfill(st + L.kown + o, src + d, ok);
-      tc::cp_async16_zfill(st + L.vown + o, src + 2 * d, ok);
-    }
-    for (int e = tid; e < 64 * KBb * 8; e += TCA_THREADS) {
-      const int t = e >> 3, c = e & 7;
-      const int64_t off = t < 128 ? (int64_t)rb[t] * ld : -1;
-      const bool ok = off >= 0;
-      const bf16* src = qkv + (ok ? off : 0) + d + gi * 64 + c * 8;
-      const uint32_t o = tc::sw128_chunk(t, c);
-      tc::cp_async16_zfill(st + L.kbase + o, src, ok);
-      tc::cp_async16_zfill(st + L.vbase + o, src + d, ok);
-    }
-    tc::cp_async_commit();
-  };
-  // S_base = Q K_base^T, S_own = Q K_own^T for head hq of item it (one thread)
-  auto issue_scores = [&](int it, int hq, int kb_base) {
-    const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
-    const uint32_t qoff = (uint32_t)(hq * dh * 2);  // head offset inside the 128-B row
-    const uint32_t idS_b = tc::make_idesc_bf16(128, kb_base > 0 ? kb_base : 16);
-    const uint32_t idS_o = tc::make_idesc_bf16(128, 128);
-    const uint64_t dq = tc::make_desc_sw128(st + L.q + qoff);
-    const uint64_t dkb = tc::make_desc_sw128(st + L.kbase + qoff);
-    const uint64_t dko = tc::make_desc_sw128(st + L.kown + qoff);
-    for (int k = 0; k < dh / 16; ++k) {  // +32 B along K = +2 in the descriptor
-      if (kb_base > 0)
-        tc::mma_bf16(tmem + TS_BASE, dq + 2 * k, dkb + 2 * k, idS_b, k != 0);
-      tc::mma_bf16(tmem + TS_OWN, dq + 2 * k, dko + 2 * k, idS_o, k != 0);
-    }
-    tc::mma_commit(&mbar[0]);
-  };
 
-  fetch_info(0);
-  fetch_info(1);
-  tc::cp_async_commit();
-  tc::cp_async_wait<0>();
-  __syncthreads();
-  prefetch(0, 0, 0);
-  prefetch(1, G == 1 ? 1 : 0, G == 1 ? 0 : 1);
-  tc::cp_async_wait<1>();
-  tc::fence_proxy_async();
-  __syncthreads();
-  if (tid == 0 && nit > 0) {
-    tc::fence_after();
-    issue_scores(0, 0, kb_of(0));
-  }
-
-  // per-tile thread state
-  bool live = false;
-  int64_t myloc = 0;
-  int kb_base = 0;
-  int nb = 0, nq = 0, wo_beg = 0;  // warp's live chunks: nb base + (nq - nb) own from wo_beg
-  int a = 0, own_lo = 0, own_cnt = 0;
-  float xn2 = 0.f, rr2 = 0.f;
-  int nloc = 0;
-  int j = 0, gi = 0;  // item it = (j, gi)
-  for (int it = 0; it < nit; ++it) {
-    const int j1 = gi + 1 == G ? j + 1 : j, g1 = gi + 1 == G ? 0 : gi + 1;  // item it + 1
-    const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
-    if (gi == 0) {
-      const uint8_t* ti = slot(j);
-      nloc = reinterpret_cast<const int32_t*>(ti + 1544)[0];
-      live = row < nloc;
-      myloc = *reinterpret_cast<const int64_t*>(ti + 1536) + row;
-      a = reinterpret_cast<const int16_t*>(ti + 1024)[row];
-      own_lo = reinterpret_cast<const int16_t*>(ti + 1280)[row];
-      own_cnt = live ? row - own_lo + 1 : 0;
-      kb_base = kb_of(j);
-      const int wb_end = (warp_max_i(a) + 15) & ~15;
-      const int w_olo = warp_min_i(live ? own_lo : 1 << 20);
-      const int w_ohi = warp_max_i(live ? row : -1);
-      wo_beg = w_olo >= 128 ? 128 : (w_olo & ~15);
-      const int wo_end = w_ohi < 0 ? 0 : ((w_ohi + 16) & ~15);
-      nb = wb_end >> 4;
-      nq = nb + max(0, (wo_end - wo_beg) >> 4);
-      xn2 = 0.f;
-      rr2 = 0.f;
-      // P columns no warp writes this tile must read as zero
-      const int pcols = (kb_base + 128) / 2;
-      const uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int c = part * 8; c < pcols; c += 32) tc::tmem_st8u(trow + TS_P + c, zero);
-      tc::tmem_wait_st();
-    }
-    ATR(12)
-    for (int hh = 0; hh < hpg; ++hh) {
-      const uint32_t koff = (uint32_t)(hh * dh * 2);  // head offset inside the 128-B row
-      tc::mbar_wait(&mbar[0], ph_s);
-      ph_s ^= 1;
+  if (warp >= TCA_SOFTMAX_WARPS) {
+    // ================= MMA warp (one thread issues every tcgen05.mma)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
+    if (warp == TCA_SOFTMAX_WARPS && lane == 0 && nit > 0) {
+      auto issue_scores = [&](int it, int hq, int kb_base) {
+        const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
+        const uint32_t qoff = (uint32_t)(hq * dh * 2);  // head offset inside the 128-B row
+        const uint32_t idS_b = tc::make_idesc_bf16(128, kb_base > 0 ? kb_base : 16);
+        const uint32_t idS_o = tc::make_idesc_bf16(128, 128);
+        const uint64_t dq = tc::make_desc_sw128(st + L.q + qoff);
+        const uint64_t dkb = tc::make_desc_sw128(st + L.kbase + qoff);
+        const uint64_t dko = tc::make_desc_sw128(st + L.kown + qoff);
+        for (int k = 0; k < dh / 16; ++k) {  // +32 B along K = +2 in the descriptor
+          if (kb_base > 0) tc::mma_bf16(tmem + TS_BASE, dq + 2 * k, dkb + 2 * k, idS_b, k != 0);
+          tc::mma_bf16(tmem + TS_OWN, dq + 2 * k, dko + 2 * k, idS_o, k != 0);
+        }
+        tc::mma_commit(s_full);
+      };
+      auto issue_pv = [&](int it, int hh, int kb_base) {
+        const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
+        const uint32_t koff = (uint32_t)(hh * dh * 2);
+        const uint32_t idO = tc::make_idesc_bf16(128, dh) | (1u << 16);
+        const uint32_t tO = tmem + TS_O + hh * dh, tA = tmem + TS_P;
+        const uint64_t db = tc::make_desc_sw128(st + L.vbase + koff);
+        const uint64_t dw = tc::make_desc_sw128(st + L.vown + koff);
+        // descriptor start field is address >> 4: 16 key rows = +128
+        for (int k16 = 0; k16 < kb_base; k16 += 16)
+          tc::mma_bf16_ts(tO, tA + (uint32_t)(k16 >> 1), db + (uint64_t)(k16 * 8), idO,
+                          k16 > 0 ? 1u : 0u);
+        for (int k16 = 0; k16 < 128; k16 += 16)
+          tc::mma_bf16_ts(tO, tA + (uint32_t)((kb_base + k16) >> 1), dw + (uint64_t)(k16 * 8),
+                          idO, (kb_base > 0 || k16 > 0) ? 1u : 0u);
+        tc::mma_commit(pv_done);
+      };
+      uint32_t ph_free = 0, ph_p = 0;
+      // S(0)
+      tc::mbar_wait(&st_full[0], 0);
       tc::fence_after();
-      ATR(0)
-      // ---- the warp's live 16-column chunks (base chunks, then own chunks)
-      // are dealt round-robin to the four warpgroups: slot i is chunk part + 4i.
-      // ONE TMEM pass loads them into registers.
-      float v[4][16];
-      bool sl[4], full[4];
-      int off[4], cnt[4];
-      uint32_t pcol[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int q = part + 4 * i;
-        sl[i] = q < nq;
-        const bool isb = q < nb;
-        const int c0 = isb ? 16 * q : wo_beg + 16 * (q - nb);
-        off[i] = isb ? c0 : c0 - own_lo;  // entry j is live iff 0 <= off + j < cnt
-        cnt[i] = isb ? a : own_cnt;
-        pcol[i] = (uint32_t)((isb ? c0 : kb_base + c0) >> 1);
-        // chunk live in full for every live row of the warp: no masking
-        full[i] = __all_sync(0xffffffffu, !live || (off[i] >= 0 && off[i] + 16 <= cnt[i]));
-        if (sl[i]) tc::tmem_ld16(trow + (isb ? TS_BASE : TS_OWN) + c0, v[i]);
+      int kb_cur = kb_of(0);
+      issue_scores(0, 0, kb_cur);
+      int it = 0, hh = 0, j = 0, gi = 0;  // head g = (it, hh), item it = (j, gi)
+      for (;;) {
+        // next head (it2, hh2)
+        int it2 = it, hh2 = hh + 1, j2 = j, gi2 = gi;
+        if (hh2 == hpg) {
+          hh2 = 0;
+          it2 = it + 1;
+          if (++gi2 == G) {
+            gi2 = 0;
+            ++j2;
+          }
+        }
+        int kb_next = kb_cur;
+        if (it2 < nit) {
+          tc::mbar_wait(s_free, ph_free);  // every warp holds S(g)
+          ph_free ^= 1;
+          if (it2 != it) {
+            tc::mbar_wait(&st_full[it2 & 1], (it2 >> 1) & 1);  // operands of item it2
+            kb_next = kb_of(j2);
+          }
+          tc::fence_after();
+          issue_scores(it2, hh2, kb_next);
+        }
+        tc::mbar_wait(p_full, ph_p);  // every warp wrote P(g)
+        ph_p ^= 1;
+        tc::fence_after();
+        issue_pv(it, hh, kb_cur);
+        if (it2 >= nit) break;
+        it = it2;
+        hh = hh2;
+        j = j2;
+        gi = gi2;
+        kb_cur = kb_next;
       }
-      tc::tmem_wait_ld();
-      ATR(1)
-      // ---- local max and sum of exp2((s - m_part) * scale * log2e)
-      float mp = -INFINITY;
+    }
+  } else {
+    // ================= softmax / epilogue warps
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;" ::: "memory");
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const float sl2 = scale * 1.4426950408889634f;
+    const uint32_t qbar = 1 + (warp & 3);  // named barrier of the row quadrant (128 threads)
+    auto qsync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory"); };
+    auto arrive = [&](uint64_t* b) {  // one arrival per warp
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(b));
+    };
+    uint32_t ph_s = 0, ph_o = 0, hc = 0;
+    ATR_DECL
+    // async copy of tile j's table into its slot (part of the caller's group)
+    auto fetch_info = [&](int j) {
+      if (j < my_tiles && tid < TINFO_BYTES / 16) {
+        const uint8_t* src = tinfo + (int64_t)(blockIdx.x + j * gridDim.x) * TINFO_BYTES;
+        tc::cp_async16(sb + L.info + (uint32_t)((j & 3) * TINFO_BYTES) + tid * 16, src + tid * 16);
+      }
+    };
+    // stage the operands of item `it` = (j, gi) (cp.async, zero-filled tails);
+    // the first item of tile j >= 1 also fetches tile j+1's table (tables 0
+    // and 1 are fetched up front)
+    auto prefetch = [&](int it, int j, int gi) {
+      if (it >= nit) return;
+      if (gi == 0 && j >= 1) fetch_info(j + 1);
+      const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
+      const int32_t* rq = reinterpret_cast<const int32_t*>(slot(j));
+      const int32_t* rb = rq + 128;
+      for (int e = tid; e < 128 * 8; e += 512) {
+        const int r = e >> 3, c = e & 7;
+        const int64_t off = (int64_t)rq[r] * ld;
+        const bool ok = off >= 0;
+        const bf16* src = qkv + (ok ? off : 0) + gi * 64 + c * 8;
+        const uint32_t o = tc::sw128_chunk(r, c);
+        tc::cp_async16_zfill(st + L.q + o, src, ok);
+        tc::cp_async16_zfill(st + L.kown + o, src + d, ok);
+        tc::cp_async16_zfill(st + L.vown + o, src + 2 * d, ok);
+      }
+      for (int e = tid; e < 64 * KBb * 8; e += 512) {
+        const int t = e >> 3, c = e & 7;
+        const int64_t off = t < 128 ? (int64_t)rb[t] * ld : -1;
+        const bool ok = off >= 0;
+        const bf16* src = qkv + (ok ? off : 0) + d + gi * 64 + c * 8;
+        const uint32_t o = tc::sw128_chunk(t, c);
+        tc::cp_async16_zfill(st + L.kbase + o, src, ok);
+        tc::cp_async16_zfill(st + L.vbase + o, src + d, ok);
+      }
+      tc::cp_async_commit();
+    };
+
+    if (nit > 0) {
+      fetch_info(0);
+      fetch_info(1);
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      asm volatile("bar.sync 5, 512;" ::: "memory");  // tables 0, 1 visible to every warp
+      prefetch(0, 0, 0);
+      prefetch(1, G == 1 ? 1 : 0, G == 1 ? 0 : 1);
+      tc::cp_async_wait<1>();
+      tc::fence_proxy_async();
+      arrive(&st_full[0]);
+    }
+
+    // per-tile thread state
+    bool live = false;
+    int64_t myloc = 0;
+    int kb_base = 0;
+    int nb = 0, nq = 0, wo_beg = 0;  // warp's live chunks: nb base + (nq - nb) own from wo_beg
+    int a = 0, own_lo = 0, own_cnt = 0;
+    float xn2 = 0.f, rr2 = 0.f;
+    int nloc = 0;
+    int j = 0, gi = 0;  // item it = (j, gi)
+    for (int it = 0; it < nit; ++it) {
+      const int j1 = gi + 1 == G ? j + 1 : j, g1 = gi + 1 == G ? 0 : gi + 1;  // item it + 1
+      if (gi == 0) {
+        // the table landed before any warp signalled this item's operands
+        tc::mbar_wait(&st_full[it & 1], (it >> 1) & 1);
+        const uint8_t* ti = slot(j);
+        nloc = reinterpret_cast<const int32_t*>(ti + 1544)[0];
+        live = row < nloc;
+        myloc = *reinterpret_cast<const int64_t*>(ti + 1536) + row;
+        a = reinterpret_cast<const int16_t*>(ti + 1024)[row];
+        own_lo = reinterpret_cast<const int16_t*>(ti + 1280)[row];
+        own_cnt = live ? row - own_lo + 1 : 0;
+        kb_base = kb_of(j);
+        const int wb_end = (warp_max_i(a) + 15) & ~15;
+        const int w_olo = warp_min_i(live ? own_lo : 1 << 20);
+        const int w_ohi = warp_max_i(live ? row : -1);
+        wo_beg = w_olo >= 128 ? 128 : (w_olo & ~15);
+        const int wo_end = w_ohi < 0 ? 0 : ((w_ohi + 16) & ~15);
+        nb = wb_end >> 4;
+        nq = nb + max(0, (wo_end - wo_beg) >> 4);
+        xn2 = 0.f;
+        rr2 = 0.f;
+        // P columns no warp writes this tile must read as zero
+        const int pcols = (kb_base + 128) / 2;
+        const uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int c = part * 8; c < pcols; c += 32) tc::tmem_st8u(trow + TS_P + c, zero);
+        tc::tmem_wait_st();
+      }
+      ATR(12)
+      for (int hh = 0; hh < hpg; ++hh) {
+        tc::mbar_wait(s_full, ph_s);
+        ph_s ^= 1;
+        tc::fence_after();
+        ATR(0)
+        // ---- the warp's live 16-column chunks (base chunks, then own chunks)
+        // are dealt round-robin to the four warpgroups: slot i is chunk
+        // part + 4i. ONE TMEM pass loads them into registers.
+        float v[4][16];
+        bool sl[4], full[4];
+        int off[4], cnt[4];
+        uint32_t pcol[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (!sl[i]) continue;
-        if (full[i]) {
+        for (int i = 0; i < 4; ++i) {
+          const int q = part + 4 * i;
+          sl[i] = q < nq;
+          const bool isb = q < nb;
+          const int c0 = isb ? 16 * q : wo_beg + 16 * (q - nb);
+          off[i] = isb ? c0 : c0 - own_lo;  // entry j is live iff 0 <= off + j < cnt
+          cnt[i] = isb ? a : own_cnt;
+          pcol[i] = (uint32_t)((isb ? c0 : kb_base + c0) >> 1);
+          // chunk live in full for every live row of the warp: no masking
+          full[i] = __all_sync(0xffffffffu, !live || (off[i] >= 0 && off[i] + 16 <= cnt[i]));
+          if (sl[i]) tc::tmem_ld16(trow + (isb ? TS_BASE : TS_OWN) + c0, v[i]);
+        }
+        tc::tmem_wait_ld();
+        tc::fence_before();
+        arrive(s_free);  // the MMA warp may overwrite S with the next head's scores
+        ATR(1)
+        // ---- local max and sum of exp2((s - m_part) * scale * log2e)
+        float mp = -INFINITY;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) mp = fmaxf(mp, v[i][q]);
-        } else {
+        for (int i = 0; i < 4; ++i) {
+          if (!sl[i]) continue;
+          if (full[i]) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) mp = fmaxf(mp, v[i][q]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const bool ok = (unsigned)(off[i] + q) < (unsigned)cnt[i];
+              v[i][q] = ok ? v[i][q] : -INFINITY;
+              mp = fmaxf(mp, v[i][q]);
+            }
+          }
+        }
+        const float mref = mp == -INFINITY ? 0.f : mp * sl2;
+        float sp = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (!sl[i]) continue;
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const bool ok = (unsigned)(off[i] + q) < (unsigned)cnt[i];
-            v[i][q] = ok ? v[i][q] : -INFINITY;
-            mp = fmaxf(mp, v[i][q]);
+            v[i][q] = ex2_approx(fmaf(v[i][q], sl2, -mref));
+            sp += v[i][q];
+          }
+        }
+        const int xb = hc & 1;
+        ++hc;
+        red[xb][part][row] = make_float2(mp, sp);
+        ATR(2)
+        qsync();
+        ATR(3)
+        float2 rq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rq[q] = red[xb][q][row];
+        const float m = fmaxf(fmaxf(rq[0].x, rq[1].x), fmaxf(rq[2].x, rq[3].x));
+        float tot = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          tot += rq[q].y > 0.f ? rq[q].y * ex2_approx((rq[q].x - m) * sl2) : 0.f;
+        const float f = sp > 0.f ? __fdividef(ex2_approx((mp - m) * sl2), tot) : 0.f;
+        ATR(4)
+        // P is rewritten only after the previous head's value MMA consumed it
+        if (hh > 0) {
+          tc::mbar_wait(pv_done, ph_o);
+          ph_o ^= 1;
+          tc::fence_after();
+        }
+        ATR(5)
+        // ---- normalised bf16 probabilities into the TMEM P tile
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (!sl[i]) continue;
+          uint32_t pk[8];
+#pragma unroll
+          for (int q = 0; q < 16; q += 2) pk[q / 2] = tc::pack_bf16(v[i][q] * f, v[i][q + 1] * f);
+          tc::tmem_st8u(trow + TS_P + pcol[i], pk);
+        }
+        tc::tmem_wait_st();
+        ATR(6)
+        tc::fence_before();
+        arrive(p_full);  // O_h = P_base V_base + P_own V_own, issued by the MMA warp
+        ATR(7)
+      }
+      // ---- the next item's operands: landed -> signal the MMA warp, whose
+      // first score MMA for it then overlaps this item's drain
+      if (it + 1 < nit) {
+        tc::cp_async_wait<0>();
+        tc::fence_proxy_async();
+        arrive(&st_full[(it + 1) & 1]);
+      }
+      ATR(8)
+      tc::mbar_wait(pv_done, ph_o);  // the item's last value MMA
+      ph_o ^= 1;
+      tc::fence_after();
+      ATR(9)
+      // ---- drain O: warpgroup `part` takes columns [16 part, 16 part + 16) of
+      // its rows into the staging tile; the quadrant's four warps then store
+      // whole 128-B row segments
+      {
+        float o[16];
+        tc::tmem_ld16(trow + TS_O + part * 16, o);  // warp-collective: every lane loads
+        tc::tmem_wait_ld();
+        uint32_t ph[8], pl[8];
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+          ph[q / 2] = tc::pack_bf16(o[q], o[q + 1]);
+          const float h0 = __uint_as_float(ph[q / 2] << 16);
+          const float h1 = __uint_as_float(ph[q / 2] & 0xffff0000u);
+          pl[q / 2] = tc::pack_bf16(o[q] - h0, o[q + 1] - h1);
+          const float r0 = __uint_as_float(pl[q / 2] << 16);
+          const float r1 = __uint_as_float(pl[q / 2] & 0xffff0000u);  // |xl|^2 (tc_vq.cuh)
+          xn2 = fmaf(o[q], o[q], fmaf(o[q + 1], o[q + 1], xn2));
+          rr2 = fmaf(r0, r0, fmaf(r1, r1, rr2));
+        }
+        const uint32_t ob = sb + L.out + (uint32_t)(row * ATT_OPITCH + part * 32);
+        tc::st_shared_v4(ob, ph[0], ph[1], ph[2], ph[3]);
+        tc::st_shared_v4(ob + 16, ph[4], ph[5], ph[6], ph[7]);
+        tc::st_shared_v4(ob + 128 * ATT_OPITCH, pl[0], pl[1], pl[2], pl[3]);
+        tc::st_shared_v4(ob + 128 * ATT_OPITCH + 16, pl[4], pl[5], pl[6], pl[7]);
+        qsync();
+        // quadrant rows 32 q .. 32 q + 31, xh then xl: 64 segments of 128 B,
+        // 8 lanes per segment, 4 segments per warp instruction
+        const int q0 = (warp & 3) * 32;
+        const int64_t loc0 = myloc - row;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int seg = (part * 4 + k) * 4 + (lane >> 3);  // 0..63
+          const int rr = q0 + (seg & 31);
+          if (rr < nloc) {
+            const uint32_t src =
+                sb + L.out + (uint32_t)((seg >> 5) * 128 * ATT_OPITCH + rr * ATT_OPITCH +
+                                        (lane & 7) * 16);
+            uint32_t w0, w1, w2, w3;
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                         : "r"(src));
+            bf16* dst =
+                ((seg >> 5) ? xl_out : xh_out) + (loc0 + rr) * d + gi * 64 + (lane & 7) * 8;
+            *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
           }
         }
       }
-      const float mref = mp == -INFINITY ? 0.f : mp * sl2;
-      float sp = 0.f;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (!sl[i]) continue;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          v[i][q] = ex2_approx(fmaf(v[i][q], sl2, -mref));
-          sp += v[i][q];
+      ATR(10)
+      if (gi == G - 1) {
+        // row norms |x|^2 and |x - xh - xl|^2, reduced over the quadrant's warps
+        nrm[0][part][row] = xn2;
+        nrm[1][part][row] = rr2;
+        qsync();
+        if (part == 0 && live) {
+          xn2_out[myloc] = ((nrm[0][0][row] + nrm[0][1][row]) + nrm[0][2][row]) + nrm[0][3][row];
+          rr2_out[myloc] = ((nrm[1][0][row] + nrm[1][1][row]) + nrm[1][2][row]) + nrm[1][3][row];
         }
       }
-      const int xb = hc & 1;
-      ++hc;
-      red[xb][part][row] = make_float2(mp, sp);
-      ATR(2)
-      tc::fence_before();
-      __syncthreads();
-      ATR(3)
-      if (tid == 0 && hh + 1 < hpg) {
-        // every warp holds its scores in registers: the next head's score
-        // MMA overlaps this head's softmax and value MMA
-        tc::fence_after();
-        issue_scores(it, hh + 1, kb_base);
-      }
-      float2 rq[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) rq[q] = red[xb][q][row];
-      const float m = fmaxf(fmaxf(rq[0].x, rq[1].x), fmaxf(rq[2].x, rq[3].x));
-      float tot = 0.f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        tot += rq[q].y > 0.f ? rq[q].y * ex2_approx((rq[q].x - m) * sl2) : 0.f;
-      const float f = sp > 0.f ? __fdividef(ex2_approx((mp - m) * sl2), tot) : 0.f;
-      // P is rewritten only after the previous head's value MMA consumed it
-      ATR(4)
-      if (hh > 0) {
-        tc::mbar_wait(&mbar[1], ph_o);
-        ph_o ^= 1;
-      }
-      ATR(5)
-      // ---- normalised bf16 probabilities into the TMEM P tile
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (!sl[i]) continue;
-        uint32_t pk[8];
-#pragma unroll
-        for (int q = 0; q < 16; q += 2) pk[q / 2] = tc::pack_bf16(v[i][q] * f, v[i][q + 1] * f);
-        tc::tmem_st8u(trow + TS_P + pcol[i], pk);
-      }
-      tc::tmem_wait_st();
-      ATR(6)
-      tc::fence_before();
-      __syncwarp();
-      // ---- O_h = P_base V_base + P_own V_own (P from TMEM, V the MN-major B
-      // operand), issued by the LAST warp to finish its P columns, so no warp
-      // idles waiting for the others
-      if (lane == 0) {
-        __threadfence_block();
-        if ((atomicAdd(p_cnt, 1u) & 15u) == 15u) {
-          __threadfence_block();
-          tc::fence_after();
-          const uint32_t idO = tc::make_idesc_bf16(128, dh) | (1u << 16);
-          const uint32_t tO = tmem + TS_O + hh * dh, tA = tmem + TS_P;
-          const uint64_t db = tc::make_desc_sw128(st + L.vbase + koff);
-          const uint64_t dw = tc::make_desc_sw128(st + L.vown + koff);
-          // descriptor start field is address >> 4: 16 key rows = +128
-          for (int k16 = 0; k16 < kb_base; k16 += 16)
-            tc::mma_bf16_ts(tO, tA + (uint32_t)(k16 >> 1), db + (uint64_t)(k16 * 8), idO,
-                            k16 > 0 ? 1u : 0u);
-          for (int k16 = 0; k16 < 128; k16 += 16)
-            tc::mma_bf16_ts(tO, tA + (uint32_t)((kb_base + k16) >> 1), dw + (uint64_t)(k16 * 8),
-                            idO, (kb_base > 0 || k16 > 0) ? 1u : 0u);
-          tc::mma_commit(&mbar[1]);
-        }
-      }
-      __syncwarp();
-      ATR(7)
+      // into this item's stage: every MMA reading it has completed
+      prefetch(it + 2, g1 + 1 == G ? j1 + 1 : j1, g1 + 1 == G ? 0 : g1 + 1);
+      ATR(11)
+      j = j1;
+      gi = g1;
     }
-    // ---- next item's operands landed -> its first score MMA runs while this
-    // item's O drains
-    if (it + 1 < nit) {
-      tc::cp_async_wait<0>();
-      tc::fence_proxy_async();
-    }
-    tc::fence_before();
-    __syncthreads();
-    if (tid == 0 && it + 1 < nit) {
-      tc::fence_after();
-      issue_scores(it + 1, 0, kb_of(j1));
-    }
-    ATR(8)
-    tc::mbar_wait(&mbar[1], ph_o);  // the item's last value MMA
-    ph_o ^= 1;
-    tc::fence_after();
-    ATR(9)
-    // ---- drain O: warpgroup `part` takes columns [16 part, 16 part + 16) of
-    // its rows into the staging tile; the quadrant's four warps then store
-    // whole 128-B row segments
-    {
-      float o[16];
-      tc::tmem_ld16(trow + TS_O + part * 16, o);  // warp-collective: every lane loads
-      tc::tmem_wait_ld();
-      uint32_t ph[8], pl[8];
-#pragma unroll
-      for (int q = 0; q < 16; q += 2) {
-        ph[q / 2] = tc::pack_bf16(o[q], o[q + 1]);
-        const float h0 = __uint_as_float(ph[q / 2] << 16);
-        const float h1 = __uint_as_float(ph[q / 2] & 0xffff0000u);
-        pl[q / 2] = tc::pack_bf16(o[q] - h0, o[q + 1] - h1);
-        const float r0 = __uint_as_float(pl[q / 2] << 16);
-        const float r1 = __uint_as_float(pl[q / 2] & 0xffff0000u);  // |xl|^2 (tc_vq.cuh)
-        xn2 = fmaf(o[q], o[q], fmaf(o[q + 1], o[q + 1], xn2));
-        rr2 = fmaf(r0, r0, fmaf(r1, r1, rr2));
-      }
-      const uint32_t ob = sb + L.out + (uint32_t)(row * ATT_OPITCH + part * 32);
-      tc::st_shared_v4(ob, ph[0], ph[1], ph[2], ph[3]);
-      tc::st_shared_v4(ob + 16, ph[4], ph[5], ph[6], ph[7]);
-      tc::st_shared_v4(ob + 128 * ATT_OPITCH, pl[0], pl[1], pl[2], pl[3]);
-      tc::st_shared_v4(ob + 128 * ATT_OPITCH + 16, pl[4], pl[5], pl[6], pl[7]);
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + (warp & 3)) : "memory");
-      // quadrant rows 32 q .. 32 q + 31, xh then xl: 64 segments of 128 B,
-      // 8 lanes per segment, 4 segments per warp instruction
-      const int q0 = (warp & 3) * 32;
-      const int64_t loc0 = myloc - row;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int seg = (part * 4 + k) * 4 + (lane >> 3);  // 0..63
-        const int rr = q0 + (seg & 31);
-        if (rr < nloc) {
-          const uint32_t src =
-              sb + L.out + (uint32_t)((seg >> 5) * 128 * ATT_OPITCH + rr * ATT_OPITCH +
-                                      (lane & 7) * 16);
-          uint32_t w0, w1, w2, w3;
-          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
-                       : "r"(src));
-          bf16* dst = ((seg >> 5) ? xl_out : xh_out) + (loc0 + rr) * d + gi * 64 + (lane & 7) * 8;
-          *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
-        }
-      }
-    }
-    ATR(10)
-    if (gi == G - 1) {
-      // row norms |x|^2 and |x - xh - xl|^2, reduced over the four warpgroups
-      nrm[0][part][row] = xn2;
-      nrm[1][part][row] = rr2;
-      __syncthreads();
-      if (part == 0 && live) {
-        xn2_out[myloc] = ((nrm[0][0][row] + nrm[0][1][row]) + nrm[0][2][row]) + nrm[0][3][row];
-        rr2_out[myloc] = ((nrm[1][0][row] + nrm[1][1][row]) + nrm[1][2][row]) + nrm[1][3][row];
-      }
-    }
-    // into this item's stage: every MMA reading it has completed
-    prefetch(it + 2, g1 + 1 == G ? j1 + 1 : j1, g1 + 1 == G ? 0 : g1 + 1);
-    ATR(11)
-    j = j1;
-    gi = g1;
-  }
 #ifdef VQNQS_ATTN_TRACE
-  if (blockIdx.x < 2 && lane == 0 && (warp == 0 || warp == 5 || warp == 10 || warp == 15))
-    printf("ATR b%d w%2d items %d: wS %llu ld %llu sm %llu bar %llu comb %llu wPV %llu P %llu arr %llu | end %llu wPVl %llu drain %llu nrm+pf %llu setup %llu\n",
-           blockIdx.x, warp, nit, atr[0], atr[1], atr[2], atr[3], atr[4], atr[5], atr[6], atr[7],
-           atr[8], atr[9], atr[10], atr[11], atr[12]);
+    if (blockIdx.x < 2 && lane == 0 && (warp == 0 || warp == 5 || warp == 10 || warp == 15))
+      printf("ATR b%d w%2d items %d: wS %llu ld %llu sm %llu bar %llu comb %llu wPV %llu P %llu arr %llu | end %llu wPVl %llu drain %llu nrm+pf %llu setup %llu\n",
+             blockIdx.x, warp, nit, atr[0], atr[1], atr[2], atr[3], atr[4], atr[5], atr[6], atr[7],
+             atr[8], atr[9], atr[10], atr[11], atr[12]);
 #endif
+  }
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem, 512);
