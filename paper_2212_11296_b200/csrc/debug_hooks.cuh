@@ -79,9 +79,11 @@ extern "C" int vqnqs_debug_vq(int64_t M, int d, const float* x, const float* cb3
     cudaMalloc(&rr2, size_t(M) * 4);
     k_vq_prep<<<sms * 4, 256>>>(dM, d, x, xh, xl, xn2, rr2);
     const CUtensorMap tmB = make_tmap_bf16(dcb, uint64_t(Q), uint64_t(d), 256);
+    VqScratch vqs;
     tc_vq(dM, M, d, xh, xl, xn2, rr2, tmB, cb32, dwn2, float(wmax * (1 + 1e-6)), Q, code,
-          n_rescored, 0, sms);
+          n_rescored, vqs, 0, sms);
     cudaDeviceSynchronize();
+    vqs.release();
     cudaFree(xh);
     cudaFree(xl);
     cudaFree(xn2);

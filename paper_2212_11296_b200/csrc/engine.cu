@@ -158,6 +158,7 @@ class EngineImpl {
   DBuf<uint8_t> cfg_stage_;
   DBuf<AttnTile> tiles_;
   DBuf<uint8_t> tinfo_;
+  VqScratch vqs_;  // deferred VQ re-scoring queue
   DBuf<int32_t> ntiles_;
   DBuf<double> out_stage_;
   DBuf<int32_t> taps_codes_;
@@ -340,6 +341,7 @@ class EngineImpl {
     cudaSetDevice(dev);
     for (void* p : allocs) cudaFree(p);
     DBufRelease();
+    vqs_.release();
     if (d_bonds) cudaFree(d_bonds);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -523,7 +525,8 @@ class EngineImpl {
             ++launches;
           }
           tc_vq(tot + 0, M, d, att_hi_.p, att_lo_.p, xn2_.p, rr2_.p, B.tmB, B.cb32, B.wn2, B.wmax, Q,
-                code_.p, d_rescored, st, sms);
+                code_.p, d_rescored, vqs_, st, sms);
+          ++launches;
         } else {
           const int LOCS = d > 384 ? 32 : 64;
           const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;

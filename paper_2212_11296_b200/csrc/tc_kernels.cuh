@@ -159,19 +159,23 @@ __global__ void k_vq_prep(const int64_t* __restrict__ Mp, int d, const float* __
 inline void tc_vq(const int64_t* Mp, int64_t Mcap, int d, const bf16* xh, const bf16* xl,
                   const float* xn2, const float* xl2, const CUtensorMap& tmB, const float* cb32,
                   const float* wn2, float wmax, int Q, int32_t* code,
-                  unsigned long long* n_rescored, cudaStream_t st, int sms) {
+                  unsigned long long* n_rescored, VqScratch& q, cudaStream_t st, int sms) {
   const size_t smem = tcv_smem_bytes(Q);
   static size_t attr = 0;
   if (attr < smem) {
     cudaFuncSetAttribute(k_tc_vq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     attr = smem;
   }
+  q.ensure(size_t(Mcap));
+  cudaMemsetAsync(q.qcount, 0, sizeof(uint32_t), st);
   const CUtensorMap tmA = make_tmap_bf16(xh, uint64_t(Mcap), uint64_t(d), 128);
   const CUtensorMap tmL = make_tmap_bf16(xl, uint64_t(Mcap), uint64_t(d), 128);
   const int64_t tiles = (Mcap + 127) / 128;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
-  k_tc_vq<<<grid, TCV_THREADS, smem, st>>>(tmA, tmL, tmB, Mp, d, xh, xl, xn2, xl2, cb32, wn2, wmax, Q,
-                                           code, n_rescored);
+  k_tc_vq<<<grid, TCV_THREADS, smem, st>>>(tmA, tmL, tmB, Mp, d, xn2, xl2, wn2, wmax, Q, code,
+                                           q.cand, q.ncand, q.qrows, q.qcount);
+  k_vq_rescore<<<sms * 2, 256, 0, st>>>(q.qcount, q.qrows, q.ncand, q.cand, xh, xl, cb32, d, Q,
+                                        code, n_rescored);
 }
 
 }  // namespace vqb

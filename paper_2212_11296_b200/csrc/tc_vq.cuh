@@ -14,10 +14,12 @@
 //            |W_j|^2 - 2 acc_j is within E = 2(|r| + d 2^-23 |x|) max|W| +
 //            slack of the exact D_j(x) - |x|^2, so every code with
 //            D~_j <= running min + 2E is kept (<= 8 per warpgroup); a single
-//            survivor is the answer, otherwise survivors are re-scored as
+//            survivor is the answer, otherwise the row and its survivors go to
+//            a queue and k_vq_rescore re-scores them as
 //            sum_c ((xh + xl)_c - W_jc)^2 in double, c ascending — the
 //            reference's own arithmetic (proj/src/model.cpp:298-303) — and the
-//            lowest index wins (strict <, :304).
+//            lowest index wins (strict <, :304). Deferring the rare re-scoring
+//            keeps it off the epilogue's critical path.
 // W is bf16-exact (the bf16 configs snap weights to bf16).
 #pragma once
 
@@ -36,7 +38,7 @@ constexpr int TCV_CAND = 8;
 constexpr int TCV_THREADS = 320;  // producer warp, MMA warp, 8 epilogue warps
 
 inline size_t tcv_smem_bytes(int Q) {
-  return 1024 + size_t(TCV_STAGES) * TCV_STAGE_BYTES + 256 + size_t(Q) * 4 + 2 * 128 * 24 + 64;
+  return 1024 + size_t(TCV_STAGES) * TCV_STAGE_BYTES + 256 + size_t(Q) * 4 + 2 * 128 * 12 + 64;
 }
 
 __device__ __forceinline__ double vq_exact_d2(const bf16* __restrict__ xh,
@@ -95,10 +97,10 @@ __device__ __forceinline__ void epi_bar() {  // the 256 epilogue threads
 __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmL,
     const __grid_constant__ CUtensorMap tmB,
-    const int64_t* __restrict__ Mp, int d, const bf16* __restrict__ xh,
-    const bf16* __restrict__ xl, const float* __restrict__ xn2g, const float* __restrict__ xl2g,
-    const float* __restrict__ cb32, const float* __restrict__ wn2_g, float wmax, int Q,
-    int32_t* __restrict__ code, unsigned long long* __restrict__ n_rescored) {
+    const int64_t* __restrict__ Mp, int d, const float* __restrict__ xn2g,
+    const float* __restrict__ xl2g, const float* __restrict__ wn2_g, float wmax, int Q, int32_t* __restrict__ code,
+    int32_t* __restrict__ cand, int32_t* __restrict__ ncand, int32_t* __restrict__ qrows,
+    uint32_t* __restrict__ qcount) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -112,8 +114,6 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
   float* red_min = wn2 + Q;                                 // [2][128]
   int* red_cnt = reinterpret_cast<int*>(red_min + 256);     // [2][128]
   int* red_jf = red_cnt + 256;                              // [2][128]
-  double* red_d = reinterpret_cast<double*>(red_jf + 256);  // [2][128]
-  int* red_j = reinterpret_cast<int*>(red_d + 256);         // [2][128]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t M = *Mp;
   const int KB = d / 64;
@@ -194,7 +194,6 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
     const int part = (warp - 2) >> 2;  // 0 or 1: columns [128 part, 128 part + 128)
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     uint32_t acc = 0;
-    unsigned long long rescored = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       const int64_t my = t * 128 + row;
       const bool live = my < M;
@@ -250,58 +249,107 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
       red_jf[part * 128 + row] = jfirst;
       epi_bar();
       const int total = red_cnt[row] + red_cnt[128 + row];
-      double best = INFINITY;
-      int jb = 0x7fffffff;
-      if (live && total != 1) {
-        const bf16* xhr = xh + my * d;
-        const bf16* xlr = xl + my * d;
-        if (total < 1000) {
-#pragma unroll 1
-          for (int i = 0; i < C.n; ++i)
-            if (C.d[i] <= gmin + w2) {
-              const double s2 = vq_exact_d2(xhr, xlr, cb32 + (int64_t)C.j[i] * d, d);
-              ++rescored;
-              if (s2 < best || (s2 == best && C.j[i] < jb)) {
-                best = s2;
-                jb = C.j[i];
-              }
-            }
+      if (live) {
+        if (total == 1) {
+          if (part == 0) code[my] = min(red_jf[row], red_jf[128 + row]);
         } else {
+          // queue the row: warpgroup 0's survivors first, then warpgroup 1's
+          const bool over = total >= 1000;
+          if (!over) {
+            int w = part == 0 ? 0 : red_cnt[row];
 #pragma unroll 1
-          for (int j = part; j < Q; j += 2) {
-            const double s2 = vq_exact_d2(xhr, xlr, cb32 + (int64_t)j * d, d);
-            ++rescored;
-            if (s2 < best || (s2 == best && j < jb)) {
-              best = s2;
-              jb = j;
-            }
+            for (int i = 0; i < C.n; ++i)
+              if (C.d[i] <= gmin + w2) cand[my * (2 * TCV_CAND) + w++] = C.j[i];
+          }
+          if (part == 0) {
+            ncand[my] = over ? -1 : total;
+            qrows[atomicAdd(qcount, 1u)] = (int32_t)my;
           }
         }
       }
-      red_d[part * 128 + row] = best;
-      red_j[part * 128 + row] = jb;
       epi_bar();
-      if (part == 0 && live) {
-        int j;
-        if (total == 1) {
-          j = min(red_jf[row], red_jf[128 + row]);
-        } else {
-          const double b0 = red_d[row], b1 = red_d[128 + row];
-          const int j0 = red_j[row], j1 = red_j[128 + row];
-          j = (b1 < b0 || (b1 == b0 && j1 < j0)) ? j1 : j0;
-        }
-        code[my] = j;
-      }
-      epi_bar();
-    }
-    if (n_rescored) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) rescored += __shfl_xor_sync(0xffffffffu, rescored, o);
-      if (lane == 0) atomicAdd(n_rescored, rescored);
     }
   }
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
+
+// Re-scoring of the queued rows: one warp per row, one lane per survivor,
+// each summing sequentially in double (c ascending) exactly like the
+// reference; overflowed rows scan the whole codebook. Ties -> lowest index.
+__global__ void __launch_bounds__(256) k_vq_rescore(
+    const uint32_t* __restrict__ qcount, const int32_t* __restrict__ qrows,
+    const int32_t* __restrict__ ncand, const int32_t* __restrict__ cand,
+    const bf16* __restrict__ xh, const bf16* __restrict__ xl, const float* __restrict__ cb32,
+    int d, int Q, int32_t* __restrict__ code, unsigned long long* __restrict__ n_rescored) {
+  const int lane = threadIdx.x & 31;
+  const int nq = (int)*qcount;
+  unsigned long long done = 0;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nq;
+       k += (gridDim.x * blockDim.x) >> 5) {
+    const int64_t row = qrows[k];
+    const int n = ncand[row];
+    const bf16* xhr = xh + row * d;
+    const bf16* xlr = xl + row * d;
+    double best = INFINITY;
+    int jb = 0x7fffffff;
+    if (n >= 0) {
+      if (lane < n) {
+        jb = cand[row * (2 * TCV_CAND) + lane];
+        best = vq_exact_d2(xhr, xlr, cb32 + (int64_t)jb * d, d);
+      }
+      done += n;
+    } else {
+#pragma unroll 1
+      for (int j = lane; j < Q; j += 32) {
+        const double s2 = vq_exact_d2(xhr, xlr, cb32 + (int64_t)j * d, d);
+        if (s2 < best) {  // j ascending per lane: strict < keeps the lowest index
+          best = s2;
+          jb = j;
+        }
+      }
+      done += Q;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, jb, o);
+      if (ob < best || (ob == best && oj < jb)) {
+        best = ob;
+        jb = oj;
+      }
+    }
+    if (lane == 0) code[row] = jb;
+  }
+  if (n_rescored && lane == 0 && done) atomicAdd(n_rescored, done);
+}
+
+// queue storage for the deferred re-scoring (device buffers, grown on demand)
+struct VqScratch {
+  int32_t* cand = nullptr;
+  int32_t* ncand = nullptr;
+  int32_t* qrows = nullptr;
+  uint32_t* qcount = nullptr;
+  size_t cap = 0;
+  void ensure(size_t rows) {
+    if (rows <= cap && qcount) return;
+    release();
+    cap = rows + rows / 4 + 1024;
+    if (cudaMalloc(&cand, cap * 2 * TCV_CAND * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&ncand, cap * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&qrows, cap * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&qcount, sizeof(uint32_t)) != cudaSuccess)
+      throw std::runtime_error("VQ re-scoring queue: out of device memory");
+  }
+  void release() {
+    if (cand) cudaFree(cand);
+    if (ncand) cudaFree(ncand);
+    if (qrows) cudaFree(qrows);
+    if (qcount) cudaFree(qcount);
+    cand = ncand = qrows = nullptr;
+    qcount = nullptr;
+    cap = 0;
+  }
+};
 
 }  // namespace vqb
