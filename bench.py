@@ -278,11 +278,16 @@ def main():
         e2e_s = float(t.item())
     clk = clocks.stop()
 
-    # roofline of the dominant kernel family (attention -> VQ stage)
+    # roofline of the dominant kernel (the tcgen05 attention): algorithmic
+    # flops = 4 d (live keys) per active location and layer (QK^T + PV over
+    # all heads), timed per launch with CUDA events on the engine stream
     peaks, peak_kind = load_peaks()
-    dom_ms, dom_flops, dom_launches = prof[0], prof[1], prof[2]
-    achieved = dom_flops / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else 0.0
+    attn_ms, attn_flops = prof[7], prof[9]
+    vq_ms, vq_flops = prof[6], prof[10]
+    achieved = attn_flops / (attn_ms / 1e3) / 1e12 if attn_ms > 0 else 0.0
+    vq_achieved = vq_flops / (vq_ms / 1e3) / 1e12 if vq_ms > 0 else 0.0
     peak = peaks.get("bf16_tflops_sustained", 1380.5)
+    ncu_ref = load_ncu_traffic()
     tot_s, q_s = led.savings()
     f_alg = falg(w, led, prof_one)
     out = {
@@ -298,14 +303,18 @@ def main():
                    "precision": w.precision, "parallelism": f"sample-shard dp{ws}",
                    "l2": "256 MB buffer written between timed steps"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
-                     "kernel": "attention->VQ stage (per layer)",
+                     "frac": achieved / peak if peak else None,
+                     "traffic": ncu_ref.get("k_tc_attention"),
+                     "kernel": "k_tc_attention (per launch = one layer of one micro-batch)",
                      "peak_source": f"{peak_kind} bf16_tflops_sustained",
-                     "stage_ms_per_step": dom_ms / args.steps,
-                     "stage_share_of_step": (dom_ms / args.steps) / ms_per_step,
-                     "attention_ms_per_step": prof[7] / args.steps,
-                     "vq_ms_per_step": prof[6] / args.steps,
-                     "vq_rescored_per_step": prof[8] / args.steps,
+                     "traffic_source": ncu_ref.get("source"),
+                     "attention_ms_per_step": attn_ms / args.steps,
+                     "attention_share_of_step": (attn_ms / args.steps) / ms_per_step,
+                     "vq": {"kernel": "k_tc_vq + k_vq_rescore", "achieved": vq_achieved,
+                            "unit": "TFLOP/s", "frac": vq_achieved / peak if peak else None,
+                            "ms_per_step": vq_ms / args.steps,
+                            "traffic": ncu_ref.get("k_tc_vq"),
+                            "rescored_rows_per_step": prof[8] / args.steps},
                      "active_locations_per_step": prof[3] / args.steps},
         "f_alg": {"flops_per_step": f_alg,
                   "fraction_of_peak": (f_alg / (ms_per_step / 1e3) / 1e12) / peak},
@@ -325,6 +334,19 @@ def main():
         print(json.dumps(out), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def load_ncu_traffic() -> dict:
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernels, from the committed `ncu --set full` capture summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return {k: v["dram_bytes_per_launch"] for k, v in d["kernels"].items()} | \
+            {"source": d.get("source")}
+    except Exception:
+        return {}
 
 
 def falg(w, led, prof) -> float:

@@ -143,7 +143,11 @@ int vqnqs_gpu_taps(vqnqs_handle* h, const uint8_t* configs, int64_t B,
 int64_t vqnqs_gpu_last_launch_count(vqnqs_handle* h);
 
 /* Per-call timings of the last call's dominant kernel family (ms, CUDA events
- * on the engine stream) and its algorithmic bytes/flops; see DESIGN.md. */
+ * on the engine stream) and its algorithmic work; see DESIGN.md. Slots:
+ * [0] attention+VQ ms  [1] their algorithmic flops  [2] launches timed
+ * [3] active locations  [4] sum U_b  [5] sum U_{b+1}  [6] VQ ms
+ * [7] attention ms  [8] VQ rows re-scored  [9] attention flops
+ * [10] VQ distance flops  [11] reserved. */
 int vqnqs_gpu_last_profile(vqnqs_handle* h, double* out, int cap);
 
 int vqnqs_gpu_destroy(vqnqs_handle* h);

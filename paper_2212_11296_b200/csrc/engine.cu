@@ -150,6 +150,7 @@ class EngineImpl {
   DBuf<int16_t> lpos_, upos_;
   DBuf<int64_t> row_aoff_, act_off_, tab_off_, Uoff_, tot_, g_res_, attw_;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> lev;  // per-layer stage events, read once per chunk
   DBuf<double> diag_, lpV_, lp_rows_;
   DBuf<unsigned long long> tkey_;
   DBuf<float> x_a, x_b, y_, att_, xn2_, rr2_;
@@ -345,6 +346,8 @@ class EngineImpl {
     if (d_bonds) cudaFree(d_bonds);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : lev)
+      if (e) cudaEventDestroy(e);
     if (own) cudaStreamDestroy(own);
     if (h_pinned_cfg) cudaFreeHost(h_pinned_cfg);
     if (h_pinned_out) cudaFreeHost(h_pinned_out);
@@ -377,9 +380,11 @@ class EngineImpl {
     nb = nbonds;
     marshall = m;
     // micro-batch size: keep the per-location working set near a fixed budget
-    const double locs = double(T) + double(nb) * 0.5 * double(T);  // ~ active per sample
+    // ~ active locations per sample: a connected row (about half the bonds)
+    // is active from its first changed token on, on average half the tokens
+    const double locs = double(T) + double(nb) * 0.25 * double(T);
     const double bytes_per_loc = double(d) * 40.0 + 64.0;
-    const double budget = 24e9;
+    const double budget = 40e9;
     S_max = int(std::clamp(budget / (locs * bytes_per_loc), 16.0, 4096.0));
   }
 
@@ -480,7 +485,7 @@ class EngineImpl {
       ++launches;
       gemm<TA>(Mb, M, 3 * d, d, h, d, nullptr, B.wqkv, B.wqkvT, B.bqkv, qkv, 3 * d, EPI_STORE,
                nullptr, 0, nullptr, st);
-      CK(cudaEventRecord(ev[0], st));
+      CK(cudaEventRecord(lev[3 * b + 0], st));
       if (use_tc_attn) {
         // tiles of whole rows (once per chunk; rows do not change across layers)
         if (b == 0) {
@@ -516,7 +521,7 @@ class EngineImpl {
             R1, T, d, dh, scale, K_.p, row_t1_.p, row_aoff_.p, act_off_.p, Icur, Uo_cur, qkv,
             att_.p);
       }
-      CK(cudaEventRecord(ev[2], st));
+      CK(cudaEventRecord(lev[3 * b + 2], st));
       {
         if (use_tc_vq) {
           if (!use_tc_attn) {
@@ -546,18 +551,7 @@ class EngineImpl {
         }
         launches += 2;
       }
-      CK(cudaEventRecord(ev[1], st));
-      {
-        // per-layer stage timing (the engine syncs per chunk anyway)
-        CK(cudaEventSynchronize(ev[1]));
-        float ms = 0.f, ma = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-        CK(cudaEventElapsedTime(&ma, ev[0], ev[2]));
-        prof[0] += ms;
-        prof[2] += 2;
-        prof[7] += ma;
-        prof[6] += ms - ma;
-      }
+      CK(cudaEventRecord(lev[3 * b + 1], st));
       if (tap_codes) {
         taps_codes_.ensure(M);
         std::vector<int32_t> hc(M);
@@ -620,10 +614,21 @@ class EngineImpl {
       CK(cudaMemcpyAsync(tap_lp->data(), lp_rows_.p, R * 8, cudaMemcpyDeviceToHost, st));
     }
     CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < L; ++b) {  // per-layer stage timing (no per-layer host sync)
+      float ms = 0.f, ma = 0.f;
+      CK(cudaEventElapsedTime(&ms, lev[3 * b + 0], lev[3 * b + 1]));
+      CK(cudaEventElapsedTime(&ma, lev[3 * b + 0], lev[3 * b + 2]));
+      prof[0] += ms;
+      prof[2] += 2;
+      prof[7] += ma;
+      prof[6] += ms - ma;
+    }
     // algorithmic work of the attention->VQ stage actually executed
     double aw = 0;
     for (int s2 = 0; s2 < S; ++s2) aw += double(haw[s2]);
     prof[1] += double(L) * (4.0 * d * aw + 2.0 * double(d) * Q * double(M));
+    prof[9] += double(L) * 4.0 * d * aw;            // attention (QK^T + PV, live keys)
+    prof[10] += double(L) * 2.0 * double(d) * Q * double(M);  // VQ distance GEMM
     prof[3] += double(M) * L;
     for (int s2 = 0; s2 < S; ++s2)
       for (int b = 0; b < L; ++b) {
@@ -642,6 +647,11 @@ class EngineImpl {
     CK(cudaMemsetAsync(d_rescored, 0, sizeof(unsigned long long), st));
     if (!ev[0])
       for (auto& e : ev) CK(cudaEventCreate(&e));
+    if (lev.size() < size_t(3 * L)) {
+      lev.resize(3 * L, nullptr);
+      for (auto& e : lev)
+        if (!e) CK(cudaEventCreate(&e));
+    }
     int64_t tap_code_pos = 0, tap_lp_pos = 0;
     for (int64_t s0 = 0; s0 < B; s0 += S_max) {
       const int S = int(std::min<int64_t>(S_max, B - s0));
