@@ -167,14 +167,17 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 __device__ __forceinline__ void mbar_fence_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// The suspend-time hint lets a waiting warp sleep until the phase completes
+// instead of re-polling (a polling waiter steals issue slots from the warps
+// sharing its scheduler).
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
   const uint32_t a = smem_u32(b);
   asm volatile(
       "{\n\t.reg .pred P;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
       "@!P bra WAIT_%=;\n\t}\n" ::"r"(a),
-      "r"(phase)
+      "r"(phase), "r"(1000000u)
       : "memory");
 }
 
