@@ -189,6 +189,8 @@ def main():
     ap.add_argument("--ref-samples", type=int, default=0)
     ap.add_argument("--warmup-ref", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true",
+                    help="skip the no-reuse (dense) regime measurement")
     ap.add_argument("--batch", type=int, default=0, help="override samples per rank")
     args = ap.parse_args()
     rank, local, ws = dist_init()
@@ -278,6 +280,34 @@ def main():
         e2e_s = float(t.item())
     clk = clocks.stop()
 
+    # the reference's no-reuse regime (dense_local_energy,
+    # proj/src/bench.cpp:19-36) on the same batch: the dedup saving in wall time
+    dense = None
+    if not args.no_dense:
+        eng.set_reuse(False)
+        step()
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        d_ms = e0.elapsed_time(e1)
+        if ws > 1:
+            t = torch.tensor([d_ms], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            d_ms = float(t.item())
+        eng.set_reuse(True)
+        dense = {"value": evals * ws / (d_ms / 1e3), "unit": UNIT, "ms_per_step": d_ms,
+                 "steps": 1, "warmup": 1,
+                 "wall_savings": d_ms / ms_per_step,
+                 "regime": "no-reuse: every connected config's full T-token forward, no shared "
+                           "prefix, no unique-row merging (proj/src/bench.cpp:19-36)"}
+
     # roofline of the dominant kernel (the tcgen05 attention): algorithmic
     # flops = 4 d (live keys) per active location and layer (QK^T + PV over
     # all heads), timed per launch with CUDA events on the engine stream
@@ -323,6 +353,7 @@ def main():
         "e2e": {"value": evals * ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(B * w.n_sites),
                 "d2h_bytes_per_step": int(3 * B * 8)},
         "gpu_launches": int(launches_per_step * args.steps),
+        "no_reuse": dense,
         "clocks": clk,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -105,6 +105,13 @@ int vqnqs_gpu_create(const vqnqs_model_desc* d, const double* const* params,
 int vqnqs_gpu_set_hamiltonian(vqnqs_handle* h, const int32_t* bonds, int nb,
                               int n_sites, int marshall);
 
+/* reuse = 1 (default): the compressed path. reuse = 0: the reference's
+ * no-reuse regime (dense_local_energy, proj/src/bench.cpp:19-36 — every
+ * connected configuration's full T-token forward, no shared prefixes, no
+ * unique-row merging); same outputs, used for the no_reuse wall-time series
+ * (proj/src/bench.cpp:193) and as an independent self-check. */
+int vqnqs_gpu_set_reuse(vqnqs_handle* h, int reuse);
+
 /* Replaces local_energies(model, h, batch, ledger)
  * (proj/include/vqnqs/trainer.hpp:76-79, proj/src/trainer.cpp:150-180).
  * configs: host [B x n_sites] bytes (0 = down, 1 = up). Outputs host arrays

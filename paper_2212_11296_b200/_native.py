@@ -49,6 +49,7 @@ SIGNATURES = {
     "vqnqs_gpu_create": (C.c_int, [C.POINTER(ModelDesc), C.POINTER(P_F64), C.c_int, C.c_int,
                                    C.c_int, C.POINTER(C.c_void_p)]),
     "vqnqs_gpu_set_hamiltonian": (C.c_int, [C.c_void_p, P_I32, C.c_int, C.c_int, C.c_int]),
+    "vqnqs_gpu_set_reuse": (C.c_int, [C.c_void_p, C.c_int]),
     "vqnqs_gpu_local_energies": (C.c_int, [C.c_void_p, P_U8, C.c_int64, P_F64, P_F64, P_F64,
                                            P_I64]),
     "vqnqs_gpu_local_energies_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64,

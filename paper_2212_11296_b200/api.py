@@ -304,6 +304,12 @@ class LocalEnergyEngine:
             lpos += int(K[s])
         return K, U, out, lps
 
+    def set_reuse(self, reuse: bool) -> None:
+        """reuse=False selects the reference's no-reuse regime
+        (dense_local_energy, proj/src/bench.cpp:19-36): same outputs, every
+        location computed."""
+        N.check(N.lib().vqnqs_gpu_set_reuse(self._h, int(bool(reuse))))
+
     def last_launch_count(self) -> int:
         return int(N.lib().vqnqs_gpu_last_launch_count(self._h))
 

@@ -106,6 +106,13 @@ int vqnqs_gpu_set_hamiltonian(vqnqs_handle* h, const int32_t* bonds, int nb, int
   });
 }
 
+int vqnqs_gpu_set_reuse(vqnqs_handle* h, int reuse) {
+  return guarded([&] {
+    if (!h) throw vqb::UsageError("null handle");
+    h->eng->set_reuse(reuse != 0);
+  });
+}
+
 int vqnqs_gpu_local_energies(vqnqs_handle* h, const uint8_t* configs, int64_t B, double* e_re,
                              double* e_im, double* logpsi, int64_t* ledger7) {
   return guarded([&] {

@@ -363,6 +363,21 @@ class EngineImpl {
     out_stage_.release(); taps_codes_.release();
   }
 
+  bool dense = false;  // no-reuse regime
+  void size_chunks() {
+    // micro-batch size: keep the per-location working set near a fixed budget.
+    // ~ active locations per sample: a connected row (about half the bonds)
+    // is active from its first changed token on, on average half the tokens;
+    // in the no-reuse regime every row is active in full
+    const double locs = double(T) + double(nb) * (dense ? 0.5 : 0.25) * double(T);
+    const double bytes_per_loc = double(d) * 40.0 + 64.0;
+    const double budget = 40e9;
+    S_max = int(std::clamp(budget / (locs * bytes_per_loc), 16.0, 4096.0));
+  }
+  void set_reuse(bool reuse) {
+    dense = !reuse;
+    size_chunks();
+  }
   void set_hamiltonian(const int32_t* bonds, int nbonds, int n_sites, bool m) {
     if (n_sites != N) throw ShapeError("configuration size != site count");
     if (nbonds < 0) throw ConfigError("negative bond count");
@@ -379,13 +394,7 @@ class EngineImpl {
     CK(cudaMemcpy(d_bonds, bonds, 2 * nbonds * sizeof(int32_t), cudaMemcpyHostToDevice));
     nb = nbonds;
     marshall = m;
-    // micro-batch size: keep the per-location working set near a fixed budget
-    // ~ active locations per sample: a connected row (about half the bonds)
-    // is active from its first changed token on, on average half the tokens
-    const double locs = double(T) + double(nb) * 0.25 * double(T);
-    const double bytes_per_loc = double(d) * 40.0 + 64.0;
-    const double budget = 40e9;
-    S_max = int(std::clamp(budget / (locs * bytes_per_loc), 16.0, 4096.0));
+    size_chunks();
   }
 
   template <typename TA>
@@ -425,7 +434,8 @@ class EngineImpl {
     row_bond_.ensure(R); row_perm_.ensure(R); row_t1_.ensure(R); row_aoff_.ensure(R); tok0_.ensure(int64_t(S) * T);
     Ucnt_.ensure(int64_t(L + 1) * S); Uoff_.ensure(int64_t(L + 1) * S); tot_.ensure(2 * (L + 2));
     int64_t* tot = tot_.p;  // [0] M total, [1] table total, [2+b] U_b total
-    k_connected<<<(S * 32 + 127) / 128, 128, 0, st>>>(S, N, g, T, nb, d_cfg, d_bonds, K_.p, diag_.p,
+    k_connected<<<(S * 32 + 127) / 128, 128, 0, st>>>(S, N, g, T, nb, int(dense), d_cfg, d_bonds,
+                                                      K_.p, diag_.p,
                                                       row_bond_.p, row_t1_.p, row_aoff_.p, Mact_.p,
                                                       tok0_.p, attw_.p, row_perm_.p);
     k_scan<<<1, 1024, 0, st>>>(S, Mact_.p, act_off_.p, tot + 0, 0);
@@ -461,7 +471,7 @@ class EngineImpl {
     int32_t* Inext = I_b.p;
     k_dedup<0><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
                                   slot_.p, lrow_.p, lpos_.p, tok0_.p, row_bond_.p, d_bonds, R1, T,
-                                  g, V, nullptr, nullptr, Icur, rep_of_.p, Ucnt_.p);
+                                  g, V, nullptr, nullptr, int(dense), Icur, rep_of_.p, Ucnt_.p);
     k_scan<<<1, 1024, 0, st>>>(S, Ucnt_.p, Uoff_.p, tot + 2, 0);
     k_embed<<<S, 256, 0, st>>>(d, R1, T, g, V, Ucnt_.p, Uoff_.p, act_off_.p, rep_of_.p, lrow_.p,
                                lpos_.p, tok0_.p, row_bond_.p, d_bonds, tok_embed, pos_embed, x_a.p);
@@ -561,7 +571,7 @@ class EngineImpl {
       }
       k_dedup<1><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
                                     slot_.p, nullptr, nullptr, nullptr, nullptr, nullptr, R1, T, g,
-                                    V, Icur, code_.p, Inext, rep_of_.p, Uc_next);
+                                    V, Icur, code_.p, int(dense), Inext, rep_of_.p, Uc_next);
       k_scan<<<1, 1024, 0, st>>>(S, Uc_next, Uo_next, tot + 3 + b, 0);
       k_build_gather<<<S, 256, 0, st>>>(Uc_next, Uo_next, Uo_cur, act_off_.p, rep_of_.p, code_.p,
                                         Icur, lpos_.p, g_code_.p, g_res_.p, upos_.p);
@@ -750,6 +760,7 @@ Engine::Engine(const vqnqs_model_desc& d, const double* const* params, int n_par
                int device)
     : p_(new EngineImpl(d, params, n_params, precision, device)) {}
 Engine::~Engine() { delete p_; }
+void Engine::set_reuse(bool reuse) { p_->set_reuse(reuse); }
 void Engine::set_hamiltonian(const int32_t* bonds, int nb, int n_sites, bool marshall) {
   p_->set_hamiltonian(bonds, nb, n_sites, marshall);
 }

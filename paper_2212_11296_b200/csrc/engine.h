@@ -65,6 +65,9 @@ class Engine {
          int device);
   ~Engine();
   void set_hamiltonian(const int32_t* bonds, int nb, int n_sites, bool marshall);
+  // reuse = false: the no-reuse (dense) regime of proj/src/bench.cpp:19-36 —
+  // every row active from position 0, every location its own unique row.
+  void set_reuse(bool reuse);
 
   struct Taps {
     int32_t* K = nullptr;       // [B]

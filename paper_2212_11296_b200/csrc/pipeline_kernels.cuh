@@ -37,7 +37,10 @@ __device__ __forceinline__ int row_token(const int32_t* tok0, const int32_t* bon
 // connected_set (proj/src/hamiltonian.cpp:41-74), one warp per sample:
 // diagonal 1/4 sum z_i z_j (exact in double: multiples of 1/4), and one row
 // per antiparallel bond in bond order (ballot + popc keeps the order).
-__global__ void k_connected(int S, int N, int g, int T, int nb, const uint8_t* __restrict__ cfg,
+// dense != 0 is the no-reuse regime (proj/src/bench.cpp:19-36): every row is
+// active from position 0 (t1 := -1), rows stay in bond order.
+__global__ void k_connected(int S, int N, int g, int T, int nb, int dense,
+                            const uint8_t* __restrict__ cfg,
                             const int32_t* __restrict__ bonds, int32_t* __restrict__ K,
                             double* __restrict__ diag, int32_t* __restrict__ row_bond,
                             int32_t* __restrict__ row_t1, int64_t* __restrict__ row_aoff,
@@ -74,7 +77,7 @@ __global__ void k_connected(int S, int N, int g, int T, int nb, const uint8_t* _
       const int zi = 2 * int(c[i]) - 1, zj = 2 * int(c[j]) - 1;
       zz += zi * zj;
       anti = c[i] != c[j];
-      t1 = min(i / g, j / g);
+      t1 = dense ? -1 : min(i / g, j / g);
       cnt = T - (t1 + 1);
     }
     const unsigned m = __ballot_sync(0xffffffffu, anti);
@@ -105,6 +108,10 @@ __global__ void k_connected(int S, int N, int g, int T, int nb, const uint8_t* _
     diag[s] = 0.25 * (double)zz;
     Mact[s] = (int32_t)aoff;
     attw[s] = aw;
+  }
+  if (dense) {  // rows keep bond order: row_aoff from the scan above
+    for (int k = lane; k < nrows; k += 32) row_perm[(int64_t)s * R1 + k] = k;
+    return;
   }
   // Re-lay the rows' active regions in order of first changed token (stable
   // counting sort by t1): rows that share t1 share their base-key range and
@@ -257,6 +264,8 @@ __global__ void __launch_bounds__(512) k_dedup(
     const int32_t* __restrict__ bonds, int R1, int T, int g, int V,
     // MODE 1 inputs
     const int32_t* __restrict__ I_in, const int32_t* __restrict__ code,
+    // no-reuse regime: every location is its own unique row
+    int dense,
     // outputs
     int32_t* __restrict__ I_out, int32_t* __restrict__ rep_of, int32_t* __restrict__ Ucnt) {
   __shared__ int wtot[32];
@@ -272,7 +281,9 @@ __global__ void __launch_bounds__(512) k_dedup(
   for (int i = tid; i < M; i += nt) {
     const int64_t loc = base + i;
     unsigned long long key;
-    if (MODE == 0) {
+    if (dense) {
+      key = (unsigned long long)i;
+    } else if (MODE == 0) {
       const int r = lrow[loc];
       const int p = lpos[loc];
       const int sidx = r / R1;
@@ -508,7 +519,7 @@ __global__ void k_eloc(int S, int R1, int T, int g, int V, double coeff,
     const int bond = row_bond[r], t1 = row_t1[r], a = t1 + 1;
     const int64_t rloc = base + row_aoff[r];
     double diff = 0.0;
-    for (int p = t1; p < T; ++p) {
+    for (int p = max(t1, 0); p < T; ++p) {  // t1 = -1 in the no-reuse regime
       const int64_t u0 = uo + I_L[base + p];
       const int64_t uk = p < a ? u0 : uo + I_L[rloc + (p - a)];
       diff += lpV[uk * V + row_token(t0, bonds, bond, g, p)] - lpV[u0 * V + t0[p]];
