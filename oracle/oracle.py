@@ -105,6 +105,7 @@ class _Common:
                                              C.c_int64, C.c_int, P_F64]
         f("dedup_log_prob").argtypes = [C.c_void_p, P_U8, C.c_int64, P_U8, P_F64]
         f("dense_log_prob").argtypes = [C.c_void_p, P_U8, C.c_int64, P_F64]
+        f("sample").argtypes = [C.c_void_p, C.c_int, C.c_uint64, P_U8, P_F64]
         f("taps").argtypes = [C.c_void_p, C.c_void_p, P_U8, P_I64, P_I32, P_F32,
                               P_F64, P_I32]
 
@@ -237,6 +238,14 @@ class OracleModel:
         self.lib._check(self.lib._f("dense_log_prob")(
             self.h, _p(configs, C.c_uint8), configs.shape[0], _p(lp, C.c_double)))
         return lp
+
+    def sample(self, count, seed):
+        """VqTransformer::sample (proj/src/model.cpp:485-525) with Rng(seed)."""
+        out = np.zeros((count, self.cfg.n_sites), np.uint8)
+        lp = np.zeros(count)
+        self.lib._check(self.lib._f("sample")(self.h, count, seed, _p(out, C.c_uint8),
+                                              _p(lp, C.c_double)))
+        return out, lp
 
     def taps(self, ham, s):
         cfg = self.cfg

@@ -242,6 +242,23 @@ void ref_zero_sz_samples(int n, int64_t start, int64_t count, uint64_t seed,
   }
 }
 
+// The reference's autoregressive sampler, VqTransformer::sample
+// (proj/src/model.cpp:485-525) with Rng(seed): configs [count x n] and the
+// recomputed log-probs (log_prob_batch, :398-426).
+int ref_sample(void* mp, int count, uint64_t seed, uint8_t* configs, double* log_probs) {
+  auto* m = static_cast<VqTransformer*>(mp);
+  return guarded([&] {
+    Rng rng(seed);
+    auto res = m->sample(count, rng);
+    const int n = m->cfg.n_sites;
+    for (int i = 0; i < count; ++i) {
+      std::copy(res.configs[size_t(i)].begin(), res.configs[size_t(i)].end(),
+                configs + int64_t(i) * n);
+      log_probs[i] = res.log_probs[size_t(i)];
+    }
+  });
+}
+
 // local_energies restated from proj/src/trainer.cpp:150-180 over the
 // reference's own local_energy_batch (proj/src/dedup.cpp:394-420).
 // logpsi[i] = 0.5 * dedup log-prob of the sample (row 0 of its connected

@@ -619,6 +619,7 @@ typedef struct {
   int32_t* codes;  /* [L*KT*H] or NULL */
   float* gaps;     /* [L*KT] or NULL */
   int32_t* I_final;
+  double* rows;    /* [KT*V] per-location log-softmax rows, or NULL */
 } taps_t;
 
 /* tokenize, proj/src/model.cpp:236-248 (little-endian groups) */
@@ -892,6 +893,9 @@ static void forward(const model_t* m, const uint8_t* configs, int64_t K,
     lp[k] = s;
   }
   if (taps && taps->I_final) memcpy(taps->I_final, x.I, (size_t)KT * 4);
+  if (taps && taps->rows)
+    for (int64_t l = 0; l < KT; ++l)
+      memcpy(taps->rows + l * V, lg + (int64_t)x.I[l] * V, (size_t)V * 8);
   free(hf);
   free(lg);
   free(toks);
@@ -913,6 +917,63 @@ int orc_dense_log_prob(void* mp, const uint8_t* configs, int64_t K, double* lp) 
   GUARD_BEGIN
   ledger_t led = {0};
   forward(mp, configs, K, NULL, 1, lp, &led, NULL);
+  GUARD_END
+}
+
+/* VqTransformer::sample, proj/src/model.cpp:485-525: T ancestral steps with
+ * Rng(seed); step t reads position t's log-softmax row of the decoder on the
+ * sampled prefix (the dense forward of the partially filled configurations:
+ * position t depends on tokens < t only, and masked keys add exact zeros),
+ * and draws by inverse CDF in sample order (:503-518). log_probs are the
+ * dense log-probs of the finished configurations (log_prob_batch, :398-426). */
+int orc_sample(void* mp, int count, uint64_t seed, uint8_t* configs, double* log_probs) {
+  GUARD_BEGIN
+  const model_t* m = mp;
+  if (count < 1) fail(1, "sample count must be >= 1");
+  const int64_t T = m->T, n = m->c.n_sites, V = m->vocab, g = m->c.group_size;
+  rng_t rng;
+  rng_init(&rng, seed);
+  int* tok = xcalloc((size_t)(count * T), sizeof(int));
+  double* rows = xcalloc((size_t)(count * T * V), 8);
+  double* lp = xcalloc((size_t)count, 8);
+  for (int64_t step = 0; step < T; ++step) {
+    for (int64_t i = 0; i < count; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        const int64_t p = j / g;
+        configs[i * n + j] = p < step ? (uint8_t)((tok[i * T + p] >> (j % g)) & 1) : 0;
+      }
+    ledger_t led = {0};
+    taps_t tp = {0};
+    tp.rows = rows;
+    forward(m, configs, count, NULL, 1, lp, &led, &tp);
+    for (int64_t i = 0; i < count; ++i) {
+      const double* row = rows + (i * T + step) * V;
+      const double u = rng_uniform(&rng);
+      double cum = 0.0;
+      int picked = -1, last_pos = 0;
+      for (int c = 0; c < m->vocab; ++c) {
+        const double pr = exp(row[c]);
+        if (pr > 0) last_pos = c;
+        cum += pr;
+        if (u < cum) {
+          picked = c;
+          break;
+        }
+      }
+      if (picked < 0) picked = last_pos; /* guard against rounding */
+      tok[i * T + step] = picked;
+    }
+  }
+  for (int64_t i = 0; i < count; ++i)
+    for (int64_t j = 0; j < n; ++j)
+      configs[i * n + j] = (uint8_t)((tok[i * T + j / g] >> (j % g)) & 1);
+  {
+    ledger_t led = {0};
+    forward(m, configs, count, NULL, 1, log_probs, &led, NULL);
+  }
+  free(tok);
+  free(rows);
+  free(lp);
   GUARD_END
 }
 

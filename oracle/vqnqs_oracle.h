@@ -45,6 +45,9 @@ int orc_local_energies_fast(void* m, void* h, const uint8_t* configs,
 int orc_dedup_log_prob(void* m, const uint8_t* configs, int64_t K,
                        const uint8_t* base, double* lp);
 int orc_dense_log_prob(void* m, const uint8_t* configs, int64_t K, double* lp);
+/* VqTransformer::sample (proj/src/model.cpp:485-525) with Rng(seed):
+ * configs [count x n_sites], log_probs [count]. */
+int orc_sample(void* m, int count, uint64_t seed, uint8_t* configs, double* log_probs);
 int orc_taps(void* m, void* h, const uint8_t* s, int64_t* U, int32_t* codes,
              float* gaps, double* lp, int32_t* I_final);
 

@@ -7,6 +7,8 @@ the Eigen shim) on seeded inputs and writes small .npz fixtures:
   golden_<case>.npz : samples, per-sample E_loc / logpsi, the ledger, and for
                       the first few samples the taps (U counts, VQ codes,
                       top-2 gaps, per-row log-probs).
+  golden_sample.npz : the reference sampler's configurations and log-probs
+                      (VqTransformer::sample) for a few seeded cases.
 
 Needs /root/reference (dev container only). The fixtures travel with the repo;
 tests/test_oracle.py checks the C restatement (oracle/_port) against them.
@@ -40,8 +42,35 @@ CASES = {
 }
 
 
+# the reference's autoregressive sampler (VqTransformer::sample,
+# proj/src/model.cpp:485-525): name -> (cfg, bf16, count, seed)
+SAMPLE_CASES = {
+    "c1_fp64": ("c1", False, 32, 7),
+    "c1_bf16": ("c1", True, 16, 11),
+    "small_open4x4": ("small_open4x4", False, 16, 3),
+}
+
+
+def make_samples(R):
+    out = {}
+    for name, (wl, bf, count, seed) in SAMPLE_CASES.items():
+        cfg = workload(wl).model if wl.startswith("c") else CASES[wl][0]
+        R.set_bf16(bf)
+        m = R.model(cfg, 0, snap_bf16=bf)
+        configs, lp = m.sample(count, seed)
+        out[f"{name}_configs"] = configs
+        out[f"{name}_log_probs"] = lp
+        out[f"{name}_seed"] = np.array(seed)
+        print("sample", name, configs.sum(1)[:6], lp[:3])
+    np.savez_compressed(os.path.join(HERE, "golden_sample.npz"), **out)
+
+
 def main():
     R = RefLib()
+    if "--sample-only" in sys.argv:
+        make_samples(R)
+        return
+    make_samples(R)
     for name, (wl, lat, bf, ns, nt) in CASES.items():
         if isinstance(wl, str):
             w = workload(wl)
