@@ -105,6 +105,18 @@ int vqnqs_gpu_create(const vqnqs_model_desc* d, const double* const* params,
 int vqnqs_gpu_set_hamiltonian(vqnqs_handle* h, const int32_t* bonds, int nb,
                               int n_sites, int marshall);
 
+/* Replaces VqTransformer::sample(count, rng) with rng = Rng(seed)
+ * (proj/src/model.cpp:485-525; proj/include/vqnqs/rng.hpp): ancestral
+ * sampling of count configurations, one position per step for all samples
+ * at once with a per-block K/V cache on the device. configs: host
+ * [count x n_sites] bytes; log_probs: host [count], the sampled
+ * configurations' log P (the reference recomputes them with log_prob_batch;
+ * here they are accumulated during the draw). Draws use the reference's
+ * uniforms in the reference's order, so a configuration differs from the
+ * reference's only where a uniform falls within rounding of a CDF step. */
+int vqnqs_gpu_sample(vqnqs_handle* h, int64_t count, uint64_t seed,
+                     uint8_t* configs, double* log_probs);
+
 /* reuse = 1 (default): the compressed path. reuse = 0: the reference's
  * no-reuse regime (dense_local_energy, proj/src/bench.cpp:19-36 — every
  * connected configuration's full T-token forward, no shared prefixes, no

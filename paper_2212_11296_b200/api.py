@@ -304,6 +304,15 @@ class LocalEnergyEngine:
             lpos += int(K[s])
         return K, U, out, lps
 
+    def sample(self, count: int, seed: int):
+        """VqTransformer::sample(count, Rng(seed)) (proj/src/model.cpp:485-525)
+        on the GPU: (configs [count x n_sites] uint8, log_probs [count])."""
+        configs = np.zeros((count, self.cfg.n_sites), np.uint8)
+        lp = np.zeros(count)
+        N.check(N.lib().vqnqs_gpu_sample(self._h, int(count), int(seed),
+                                         N.ptr(configs, C.c_uint8), N.ptr(lp, C.c_double)))
+        return configs, lp
+
     def set_reuse(self, reuse: bool) -> None:
         """reuse=False selects the reference's no-reuse regime
         (dense_local_energy, proj/src/bench.cpp:19-36): same outputs, every

@@ -106,6 +106,14 @@ int vqnqs_gpu_set_hamiltonian(vqnqs_handle* h, const int32_t* bonds, int nb, int
   });
 }
 
+int vqnqs_gpu_sample(vqnqs_handle* h, int64_t count, uint64_t seed, uint8_t* configs,
+                     double* log_probs) {
+  return guarded([&] {
+    if (!h || !configs || !log_probs) throw vqb::UsageError("null argument");
+    h->eng->sample(count, seed, configs, log_probs);
+  });
+}
+
 int vqnqs_gpu_set_reuse(vqnqs_handle* h, int reuse) {
   return guarded([&] {
     if (!h) throw vqb::UsageError("null handle");

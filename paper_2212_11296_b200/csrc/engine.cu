@@ -27,6 +27,7 @@
 #include "simt_kernels.cuh"
 #include "tc_attention.cuh"
 #include "tc_kernels.cuh"
+#include "sampler_kernels.cuh"
 
 namespace vqb {
 
@@ -44,6 +45,10 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
   void ensure(size_t want) {
     if (want <= n) return;
     if (p) cudaFree(p);
@@ -720,6 +725,150 @@ class EngineImpl {
     prof[8] = double(resc);
   }
 
+  // ---------------------------------------------------------------- sampler
+  template <typename TA>
+  void sample_chunk(int B, const double* d_u, int32_t* d_tok, double* d_lp, cudaStream_t st) {
+    const size_t es = esz();
+    DBuf<float> x, ya, att;
+    DBuf<char> h, qkv, f1, kc, vc;
+    DBuf<bf16> xh, xl;
+    DBuf<float> xn2, rr2;
+    DBuf<int32_t> code;
+    DBuf<int64_t> dB, iota;
+    DBuf<int16_t> pos;
+    DBuf<double> lpv;
+    x.ensure(size_t(B) * d);
+    ya.ensure(size_t(B) * d);
+    att.ensure(size_t(B) * d);
+    h.ensure(size_t(B) * d * es);
+    qkv.ensure(size_t(B) * 3 * d * es);
+    f1.ensure(size_t(B) * 4 * d * es);
+    kc.ensure(size_t(L) * B * T * d * es);
+    vc.ensure(size_t(L) * B * T * d * es);
+    code.ensure(B);
+    dB.ensure(1);
+    iota.ensure(B);
+    pos.ensure(B);
+    lpv.ensure(size_t(B) * V);
+    if (use_tc_vq) {
+      xh.ensure(size_t(B) * d);
+      xl.ensure(size_t(B) * d);
+      xn2.ensure(B);
+      rr2.ensure(B);
+    }
+    const int64_t b64 = B;
+    CK(cudaMemcpyAsync(dB.p, &b64, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    k_iota64<<<(B + 255) / 256, 256, 0, st>>>(B, iota.p);
+    const int lnGrid = sms * 8;
+    const float scale = float(1.0 / std::sqrt(double(dh)));
+    TA* hp = reinterpret_cast<TA*>(h.p);
+    TA* qp = reinterpret_cast<TA*>(qkv.p);
+    TA* fp = reinterpret_cast<TA*>(f1.p);
+    const int awpb = 4;
+    const size_t asmem = size_t(awpb) * (dh + T) * sizeof(float);
+    if (asmem > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_dec_attention<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              int(asmem)));
+    launches += 2;
+    for (int t = 0; t < T; ++t) {
+      k_dec_embed<<<B, 128, 0, st>>>(B, d, T, V, t, d_tok, tok_embed, pos_embed, x.p);
+      k_fill_i16<<<(B + 255) / 256, 256, 0, st>>>(B, int16_t(t), pos.p);
+      launches += 2;
+      float* xc = x.p;
+      float* xn = ya.p;
+      for (int b = 0; b < L; ++b) {
+        const DevBlock& Bk = blk[b];
+        k_layernorm<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, xc, Bk.ln1_g, Bk.ln1_b, hp);
+        gemm<TA>(dB.p, B, 3 * d, d, hp, d, nullptr, Bk.wqkv, Bk.wqkvT, Bk.bqkv, qp, 3 * d,
+                 EPI_STORE, nullptr, 0, nullptr, st);
+        TA* kcb = reinterpret_cast<TA*>(kc.p) + size_t(b) * B * T * d;
+        TA* vcb = reinterpret_cast<TA*>(vc.p) + size_t(b) * B * T * d;
+        const int64_t jobs = int64_t(B) * nh;
+        k_dec_attention<TA><<<int((jobs + awpb - 1) / awpb), 32 * awpb, asmem, st>>>(
+            B, d, nh, T, t, scale, qp, kcb, vcb, att.p);
+        launches += 2;
+        if (use_tc_vq) {
+          k_vq_prep<<<sms * 8, 256, 0, st>>>(dB.p, d, att.p, xh.p, xl.p, xn2.p, rr2.p);
+          tc_vq(dB.p, B, d, xh.p, xl.p, xn2.p, rr2.p, Bk.tmB, Bk.cb32, Bk.wn2, Bk.wmax, Q,
+                code.p, nullptr, vqs_, st, sms);
+          launches += 3;
+        } else {
+          const int LOCS = d > 384 ? 32 : 64;
+          const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;
+          const int vgrid = int(std::max<int64_t>(1, std::min<int64_t>((B + LOCS - 1) / LOCS,
+                                                                        int64_t(sms) * 4)));
+          if (LOCS == 64) {
+            if (vsmem > 48 * 1024)
+              CK(cudaFuncSetAttribute(k_vq<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(vsmem)));
+            k_vq<64><<<vgrid, 256, vsmem, st>>>(dB.p, d, att.p, Bk.cb32, Q, code.p);
+          } else {
+            if (vsmem > 48 * 1024)
+              CK(cudaFuncSetAttribute(k_vq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(vsmem)));
+            k_vq<32><<<vgrid, 256, vsmem, st>>>(dB.p, d, att.p, Bk.cb32, Q, code.p);
+          }
+          ++launches;
+        }
+        // continuation (proj/src/dedup.cpp:246-267) from the per-code Wo table
+        k_cont_ln<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, xc, iota.p, code.p, Bk.pwo, Bk.ln2_g,
+                                              Bk.ln2_b, y_.p, hp);
+        ++launches;
+        gemm<TA>(dB.p, B, 4 * d, d, hp, d, nullptr, Bk.w1, Bk.w1T, Bk.b1, fp, 4 * d, EPI_GELU,
+                 nullptr, 0, nullptr, st);
+        gemm<TA>(dB.p, B, d, 4 * d, fp, 4 * d, nullptr, Bk.w2, Bk.w2T, Bk.b2, xn, d, EPI_RESID,
+                 y_.p, d, nullptr, st);
+        std::swap(xc, xn);
+      }
+      k_layernorm<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, xc, lnf_g, lnf_b, hp);
+      k_head<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, V, lastV, T, hp, static_cast<const TA*>(head_w),
+                                         head_b, pos.p, lpv.p);
+      k_dec_sample<<<(B + 127) / 128, 128, 0, st>>>(B, T, V, t, lpv.p, d_u, d_tok, d_lp);
+      launches += 3;
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+  }
+
+  void sample(int64_t count, uint64_t seed, uint8_t* cfg_out, double* lp_out) {
+    CK(cudaSetDevice(dev));
+    launches = 0;
+    cudaStream_t st = own;
+    // the reference's draws: step-major, then sample index (model.cpp:497-518)
+    std::vector<double> hu(size_t(count) * T);
+    rng_uniforms(seed, int64_t(hu.size()), hu.data());
+    // micro-batches of samples (K/V cache: 2 L T d per sample)
+    const double per = double(L) * T * d * esz() * 2 + double(d) * 60;
+    const int64_t Bmax = std::max<int64_t>(1, std::min<int64_t>(int64_t(24e9 / per), 65536));
+    DBuf<double> du, dlp;
+    DBuf<int32_t> dtok;
+    DBuf<uint8_t> dcfg;
+    for (int64_t s0 = 0; s0 < count; s0 += Bmax) {
+      const int B = int(std::min<int64_t>(Bmax, count - s0));
+      std::vector<double> cu(size_t(B) * T);
+      for (int t = 0; t < T; ++t)
+        std::memcpy(cu.data() + size_t(t) * B, hu.data() + size_t(t) * count + s0,
+                    size_t(B) * sizeof(double));
+      du.ensure(cu.size());
+      dlp.ensure(B);
+      dtok.ensure(size_t(B) * T);
+      dcfg.ensure(size_t(B) * N);
+      y_.ensure(size_t(B) * d);
+      CK(cudaMemcpyAsync(du.p, cu.data(), cu.size() * sizeof(double), cudaMemcpyHostToDevice,
+                         st));
+      if (prec == VQNQS_PREC_BF16)
+        sample_chunk<bf16>(B, du.p, dtok.p, dlp.p, st);
+      else
+        sample_chunk<float>(B, du.p, dtok.p, dlp.p, st);
+      k_detokenize<<<int((int64_t(B) * N + 255) / 256), 256, 0, st>>>(B, N, g, T, dtok.p, dcfg.p);
+      ++launches;
+      CK(cudaMemcpyAsync(cfg_out + s0 * N, dcfg.p, size_t(B) * N, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(lp_out + s0, dlp.p, size_t(B) * sizeof(double), cudaMemcpyDeviceToHost,
+                         st));
+      CK(cudaStreamSynchronize(st));
+    }
+  }
+
   void run_host(const uint8_t* configs, int64_t B, double* e_re, double* e_im, double* logpsi,
                 int64_t* ledger7, Engine::Taps* taps) {
     CK(cudaSetDevice(dev));
@@ -768,6 +917,10 @@ void Engine::run_device(const uint8_t* d_configs, int64_t B, double* d_e, double
                         int64_t* ledger7, void* stream, Taps* taps) {
   p_->run_device(d_configs, B, d_e, d_logpsi, ledger7,
                  stream ? static_cast<cudaStream_t>(stream) : p_->own, taps);
+}
+void Engine::sample(int64_t count, uint64_t seed, uint8_t* configs, double* log_probs) {
+  if (count < 1) throw ConfigError("sample count must be >= 1");
+  p_->sample(count, seed, configs, log_probs);
 }
 void Engine::run_host(const uint8_t* configs, int64_t B, double* e_re, double* e_im,
                       double* logpsi, int64_t* ledger7, Taps* taps) {

@@ -50,6 +50,8 @@ std::vector<ParamSpec> param_layout(const vqnqs_model_desc& c);
 void init_params(const vqnqs_model_desc& c, uint64_t seed, bool snap, double* const* out);
 std::vector<int32_t> build_lattice(int lx, int ly, bool periodic);
 void zero_sz_samples(int n, int64_t start, int64_t count, uint64_t seed, uint8_t* out);
+// n consecutive Rng(seed).uniform() draws (proj/include/vqnqs/rng.hpp:22).
+void rng_uniforms(uint64_t seed, int64_t n, double* out);
 
 // Host-side restatement of the reference ledger for one sample
 // (proj/src/flops.cpp:29-72 with the opcost formulas of
@@ -84,6 +86,9 @@ class Engine {
   // Host batch (pinned staging inside).
   void run_host(const uint8_t* configs, int64_t B, double* e_re, double* e_im, double* logpsi,
                 int64_t* ledger7, Taps* taps);
+  // The autoregressive sampler (VqTransformer::sample, proj/src/model.cpp:
+  // 485-525) with Rng(seed): configs [count x n] and log-probs [count], host.
+  void sample(int64_t count, uint64_t seed, uint8_t* configs, double* log_probs);
   int64_t last_launches() const;
   int last_profile(double* out, int cap) const;
   const vqnqs_model_desc& desc() const;

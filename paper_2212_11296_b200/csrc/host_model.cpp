@@ -190,6 +190,11 @@ std::vector<int32_t> build_lattice(int lx, int ly, bool periodic) {
   return b;
 }
 
+void rng_uniforms(uint64_t seed, int64_t n, double* out) {
+  Rng r(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.uniform();
+}
+
 void zero_sz_samples(int n, int64_t start, int64_t count, uint64_t seed, uint8_t* out) {
   const Rng master(seed);
   for (int64_t i = 0; i < count; ++i) {
