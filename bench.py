@@ -189,6 +189,7 @@ def main():
     ap.add_argument("--ref-samples", type=int, default=0)
     ap.add_argument("--warmup-ref", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sampler", action="store_true", help="skip the sampler measurement")
     ap.add_argument("--no-dense", action="store_true",
                     help="skip the no-reuse (dense) regime measurement")
     ap.add_argument("--batch", type=int, default=0, help="override samples per rank")
@@ -280,6 +281,19 @@ def main():
         e2e_s = float(t.item())
     clk = clocks.stop()
 
+    # the autoregressive sampler on the GPU (VqTransformer::sample,
+    # proj/src/model.cpp:485-525): B draws, host in/out
+    sampler = None
+    if not args.no_sampler:
+        eng.sample(64, 1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, lp_s = eng.sample(B, 1000 + rank)
+        dt = time.perf_counter() - t0
+        sampler = {"value": B * ws / dt, "unit": "samples/s", "count_per_rank": B,
+                   "seconds": dt, "mean_log_prob": float(np.mean(lp_s)),
+                   "method": "one position per step for all samples, per-block K/V cache"}
+
     # the reference's no-reuse regime (dense_local_energy,
     # proj/src/bench.cpp:19-36) on the same batch: the dedup saving in wall time
     dense = None
@@ -354,6 +368,7 @@ def main():
                 "d2h_bytes_per_step": int(3 * B * 8)},
         "gpu_launches": int(launches_per_step * args.steps),
         "no_reuse": dense,
+        "sampler": sampler,
         "clocks": clk,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
