@@ -113,8 +113,10 @@ int vqnqs_gpu_set_hamiltonian(vqnqs_handle* h, const int32_t* bonds, int nb,
  * configurations' log P (the reference recomputes them with log_prob_batch;
  * here they are accumulated during the draw). Draws use the reference's
  * uniforms in the reference's order, so a configuration differs from the
- * reference's only where a uniform falls within rounding of a CDF step. */
-int vqnqs_gpu_sample(vqnqs_handle* h, int64_t count, uint64_t seed,
+ * reference's only where a uniform falls within rounding of a CDF step.
+ * skip = uniforms of the same Rng(seed) stream already consumed (count x T
+ * per earlier batch), so consecutive calls continue one stream. */
+int vqnqs_gpu_sample(vqnqs_handle* h, int64_t count, uint64_t seed, uint64_t skip,
                      uint8_t* configs, double* log_probs);
 
 /* reuse = 1 (default): the compressed path. reuse = 0: the reference's

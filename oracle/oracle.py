@@ -106,6 +106,12 @@ class _Common:
         f("dedup_log_prob").argtypes = [C.c_void_p, P_U8, C.c_int64, P_U8, P_F64]
         f("dense_log_prob").argtypes = [C.c_void_p, P_U8, C.c_int64, P_F64]
         f("sample").argtypes = [C.c_void_p, C.c_int, C.c_uint64, P_U8, P_F64]
+        if self.prefix == "ref_":  # wire formats: the reference's own code
+            f("save_checkpoint").argtypes = [C.c_void_p, C.c_char_p]
+            f("load_checkpoint").restype = C.c_void_p
+            f("load_checkpoint").argtypes = [C.c_char_p]
+            f("measure_and_emit").argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                              C.c_uint64, C.c_double, C.c_char_p]
         f("taps").argtypes = [C.c_void_p, C.c_void_p, P_U8, P_I64, P_I32, P_F32,
                               P_F64, P_I32]
 
@@ -128,6 +134,13 @@ class _Common:
     def model(self, cfg, seed=0, snap_bf16=False):
         d = desc_from(cfg)
         h = self._f("model_create")(C.byref(d), seed, int(snap_bf16))
+        if not h:
+            raise OracleError(1, self._f("last_error")().decode())
+        return OracleModel(self, h, cfg)
+
+    def load_checkpoint(self, path, cfg):
+        """The reference's load_checkpoint (proj/src/checkpoint.cpp:79-124)."""
+        h = self._f("load_checkpoint")(str(path).encode())
         if not h:
             raise OracleError(1, self._f("last_error")().decode())
         return OracleModel(self, h, cfg)
@@ -179,6 +192,16 @@ class OracleModel:
             self.lib._f("model_destroy")(self.h)
         except Exception:
             pass
+
+    def save_checkpoint(self, path):
+        self.lib._check(self.lib._f("save_checkpoint")(self.h, str(path).encode()))
+
+    def measure_and_emit(self, ham, samples_per_batch, batches, seed, directory,
+                         reference_per_site=float("nan")):
+        """measure_flops + emit_table (proj/src/bench.cpp:65-124, 270-290)."""
+        self.lib._check(self.lib._f("measure_and_emit")(
+            self.h, ham.h, samples_per_batch, batches, seed, reference_per_site,
+            str(directory).encode()))
 
     def params(self):
         """[(name, float64 array)] in parameters() order."""

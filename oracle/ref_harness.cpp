@@ -18,7 +18,11 @@
 //   * a "taps" pass that re-composes dedup_log_prob (proj/src/dedup.cpp:272-323)
 //     from the public dedup.hpp functions to expose per-layer unique counts,
 //     per-location VQ codes and the top-2 relative distance gap, and checks
-//     that its log-probs equal dedup_log_prob's bit for bit.
+//     that its log-probs equal dedup_log_prob's bit for bit;
+//   * the checkpoint wire format (proj/src/checkpoint.cpp, linked with the
+//     nlohmann json single header found in this image) and the measurement
+//     report (measure_flops + emit_table, proj/src/bench.cpp) for the
+//     SURVEY §8(f) rank-4 wire formats.
 #include <atomic>
 #include <cmath>
 #include <complex>
@@ -30,6 +34,8 @@
 
 #include <Eigen/Dense>
 
+#include "vqnqs/bench.hpp"
+#include "vqnqs/checkpoint.hpp"
 #include "vqnqs/dedup.hpp"
 #include "vqnqs/flops.hpp"
 #include "vqnqs/hamiltonian.hpp"
@@ -240,6 +246,28 @@ void ref_zero_sz_samples(int n, int64_t start, int64_t count, uint64_t seed,
       std::swap(s[j], s[t]);
     }
   }
+}
+
+// save_checkpoint / load_checkpoint (proj/src/checkpoint.cpp:53-126)
+int ref_save_checkpoint(void* mp, const char* path) {
+  return guarded([&] { save_checkpoint(*static_cast<VqTransformer*>(mp), path); });
+}
+void* ref_load_checkpoint(const char* path) {
+  VqTransformer* m = nullptr;
+  int st = guarded([&] { m = new VqTransformer(load_checkpoint(path)); });
+  return st == 0 ? m : nullptr;
+}
+
+// measure_flops (proj/src/bench.cpp:65-124) with Rng(seed), then
+// emit_table({report}, dir) (:270-290): report.csv / report.json in dir.
+int ref_measure_and_emit(void* mp, void* hp, int samples_per_batch, int batches, uint64_t seed,
+                         double reference_per_site, const char* dir) {
+  return guarded([&] {
+    Rng rng(seed);
+    auto rep = measure_flops(*static_cast<VqTransformer*>(mp), *static_cast<HamiltonianModel*>(hp),
+                             samples_per_batch, batches, rng, reference_per_site);
+    emit_table({rep}, dir);
+  });
 }
 
 // The reference's autoregressive sampler, VqTransformer::sample

@@ -216,6 +216,7 @@ class LocalEnergyEngine:
         if ham.n_sites() != model.cfg.n_sites:
             raise ShapeError("configuration size != site count")
         self.cfg = model.cfg
+        self.ham = ham
         self.precision = precision
         self.device = device
         desc = N.desc_of(model.cfg)
@@ -304,12 +305,18 @@ class LocalEnergyEngine:
             lpos += int(K[s])
         return K, U, out, lps
 
-    def sample(self, count: int, seed: int):
+    def system_name(self) -> str:
+        """system_name, proj/src/bench.cpp:46-55."""
+        return f"{self.ham.kind} " + "x".join(str(x) for x in self.ham.lattice.dims)
+
+    def sample(self, count: int, seed: int, skip: int = 0):
         """VqTransformer::sample(count, Rng(seed)) (proj/src/model.cpp:485-525)
-        on the GPU: (configs [count x n_sites] uint8, log_probs [count])."""
+        on the GPU: (configs [count x n_sites] uint8, log_probs [count]).
+        skip = uniforms of the Rng(seed) stream already consumed by earlier
+        batches (count x seq_len each)."""
         configs = np.zeros((count, self.cfg.n_sites), np.uint8)
         lp = np.zeros(count)
-        N.check(N.lib().vqnqs_gpu_sample(self._h, int(count), int(seed),
+        N.check(N.lib().vqnqs_gpu_sample(self._h, int(count), int(seed), int(skip),
                                          N.ptr(configs, C.c_uint8), N.ptr(lp, C.c_double)))
         return configs, lp
 

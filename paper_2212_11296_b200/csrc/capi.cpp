@@ -106,11 +106,11 @@ int vqnqs_gpu_set_hamiltonian(vqnqs_handle* h, const int32_t* bonds, int nb, int
   });
 }
 
-int vqnqs_gpu_sample(vqnqs_handle* h, int64_t count, uint64_t seed, uint8_t* configs,
-                     double* log_probs) {
+int vqnqs_gpu_sample(vqnqs_handle* h, int64_t count, uint64_t seed, uint64_t skip,
+                     uint8_t* configs, double* log_probs) {
   return guarded([&] {
     if (!h || !configs || !log_probs) throw vqb::UsageError("null argument");
-    h->eng->sample(count, seed, configs, log_probs);
+    h->eng->sample(count, seed, skip, configs, log_probs);
   });
 }
 

@@ -830,13 +830,14 @@ class EngineImpl {
     CK(cudaStreamSynchronize(st));
   }
 
-  void sample(int64_t count, uint64_t seed, uint8_t* cfg_out, double* lp_out) {
+  void sample(int64_t count, uint64_t seed, uint64_t skip, uint8_t* cfg_out, double* lp_out) {
     CK(cudaSetDevice(dev));
     launches = 0;
     cudaStream_t st = own;
     // the reference's draws: step-major, then sample index (model.cpp:497-518)
-    std::vector<double> hu(size_t(count) * T);
+    std::vector<double> hu(size_t(skip) + size_t(count) * T);
     rng_uniforms(seed, int64_t(hu.size()), hu.data());
+    hu.erase(hu.begin(), hu.begin() + int64_t(skip));
     // micro-batches of samples (K/V cache: 2 L T d per sample)
     const double per = double(L) * T * d * esz() * 2 + double(d) * 60;
     const int64_t Bmax = std::max<int64_t>(1, std::min<int64_t>(int64_t(24e9 / per), 65536));
@@ -918,9 +919,10 @@ void Engine::run_device(const uint8_t* d_configs, int64_t B, double* d_e, double
   p_->run_device(d_configs, B, d_e, d_logpsi, ledger7,
                  stream ? static_cast<cudaStream_t>(stream) : p_->own, taps);
 }
-void Engine::sample(int64_t count, uint64_t seed, uint8_t* configs, double* log_probs) {
+void Engine::sample(int64_t count, uint64_t seed, uint64_t skip, uint8_t* configs,
+                    double* log_probs) {
   if (count < 1) throw ConfigError("sample count must be >= 1");
-  p_->sample(count, seed, configs, log_probs);
+  p_->sample(count, seed, skip, configs, log_probs);
 }
 void Engine::run_host(const uint8_t* configs, int64_t B, double* e_re, double* e_im,
                       double* logpsi, int64_t* ledger7, Taps* taps) {

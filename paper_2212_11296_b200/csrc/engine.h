@@ -88,7 +88,9 @@ class Engine {
                 int64_t* ledger7, Taps* taps);
   // The autoregressive sampler (VqTransformer::sample, proj/src/model.cpp:
   // 485-525) with Rng(seed): configs [count x n] and log-probs [count], host.
-  void sample(int64_t count, uint64_t seed, uint8_t* configs, double* log_probs);
+  // skip: uniforms of the Rng(seed) stream already consumed (a later batch of
+  // the same stream, as measure_flops draws, proj/src/bench.cpp:84-85).
+  void sample(int64_t count, uint64_t seed, uint64_t skip, uint8_t* configs, double* log_probs);
   int64_t last_launches() const;
   int last_profile(double* out, int cap) const;
   const vqnqs_model_desc& desc() const;

@@ -9,6 +9,8 @@ the Eigen shim) on seeded inputs and writes small .npz fixtures:
                       top-2 gaps, per-row log-probs).
   golden_sample.npz : the reference sampler's configurations and log-probs
                       (VqTransformer::sample) for a few seeded cases.
+  ckpt_c1.vqnqs, report_c1/report.{csv,json} : the reference's checkpoint
+                      file and measurement report (the §8(f) wire formats).
 
 Needs /root/reference (dev container only). The fixtures travel with the repo;
 tests/test_oracle.py checks the C restatement (oracle/_port) against them.
@@ -65,12 +67,27 @@ def make_samples(R):
     np.savez_compressed(os.path.join(HERE, "golden_sample.npz"), **out)
 
 
+def make_wire(R):
+    """The reference's checkpoint file for the c1 model (seed 0) and its
+    measurement report (measure_flops, 8 x 2 samples, Rng(5), periodic 4x4)."""
+    cfg = workload("c1").model
+    R.set_bf16(False)
+    m = R.model(cfg, 0)
+    m.save_checkpoint(os.path.join(HERE, "ckpt_c1.vqnqs"))
+    m.measure_and_emit(R.hamiltonian("grid_periodic", 4, 4), 8, 2, 5,
+                       os.path.join(HERE, "report_c1"))
+
+
 def main():
     R = RefLib()
     if "--sample-only" in sys.argv:
         make_samples(R)
         return
+    if "--wire-only" in sys.argv:
+        make_wire(R)
+        return
     make_samples(R)
+    make_wire(R)
     for name, (wl, lat, bf, ns, nt) in CASES.items():
         if isinstance(wl, str):
             w = workload(wl)
