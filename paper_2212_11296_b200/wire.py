@@ -158,7 +158,7 @@ def measure_flops(engine: LocalEnergyEngine, samples_per_batch: int, batches: in
         led = Ledger()
         e, _ = engine.local_energies(configs, led)
         total += led
-        esum += float(np.sum(e))
+        esum += float(np.real(np.sum(e)))  # Re E (bench.cpp:90)
         count += len(e)
     rep.flops_dense = total.total_dense()
     rep.flops_dedup = total.total_dedup()
