@@ -170,13 +170,21 @@ __global__ void __launch_bounds__(128, 1) k_tc_gemm(
 // K-blocks into a 4-stage ring, warp 1 issues tcgen05.mma into one of two
 // BN-column TMEM accumulators, warps 2-9 (two warpgroups, BN/2 columns each)
 // drain the other accumulator through the fused epilogue, so loads, MMAs and
-// epilogues of consecutive tiles overlap.
-constexpr int TCW_STAGES = 4;
+// epilogues of consecutive tiles overlap. The epilogue stages 64-column
+// slabs of its 32 rows in a warp-private shared tile and writes (and, for the
+// residual epilogue, reads) whole 128/256-byte row segments.
 constexpr int TCW_THREADS = 320;
+constexpr int TCW_STG_PITCH = 68;  // floats per staged row (64 + 4: conflict-free 16-B writes)
+constexpr uint32_t TCW_STG_BYTES = 8 * 32 * TCW_STG_PITCH * 4;
+
+template <int BN>
+constexpr int tcw_stages() {
+  return BN >= 256 ? 3 : 4;
+}
 
 template <int BN>
 constexpr size_t tcw_smem_bytes() {
-  return 1024 + size_t(TCW_STAGES) * (128 * 128 + BN * 128) + 256;
+  return 1024 + size_t(tcw_stages<BN>()) * (128 * 128 + BN * 128) + TCW_STG_BYTES + 256;
 }
 
 template <int BN, int EPI>
@@ -187,8 +195,10 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc_gemm_ws(
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
+  constexpr int TCW_STAGES = tcw_stages<BN>();
   constexpr uint32_t A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TCW_STAGES * STAGE);
+  float* stg_all = reinterpret_cast<float*>(smem + TCW_STAGES * STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TCW_STAGES * STAGE + TCW_STG_BYTES);
   uint64_t* empty = full + TCW_STAGES;
   uint64_t* acc_full = empty + TCW_STAGES;
   uint64_t* acc_empty = acc_full + 2;
@@ -257,52 +267,68 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc_gemm_ws(
       }
     }
   } else {
-    const int row = (warp & 3) * 32 + lane;
     const int part = (warp - 2) >> 2;  // columns [part*BN/2, part*BN/2 + BN/2)
-    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const int q0 = (warp & 3) * 32;     // this warp's TMEM lanes = tile rows q0..q0+31
+    const uint32_t trow = tmem + ((uint32_t)q0 << 16);
+    float* stg = stg_all + (warp - 2) * 32 * TCW_STG_PITCH;
     uint32_t acc = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++acc) {
       const uint32_t b = acc & 1;
-      const int64_t m = (t / tilesN) * 128 + row;
+      const int64_t m0 = (t / tilesN) * 128 + q0;
       const int n0 = int(t % tilesN) * BN;
       tc::mbar_wait(&acc_full[b], (acc >> 1) & 1);
       tc::fence_after();
-      for (int c0 = part * (BN / 2); c0 < (part + 1) * (BN / 2); c0 += 16) {
-        float v[16];
-        tc::tmem_ld16(trow + b * BN + c0, v);
-        tc::tmem_wait_ld();
-        if (m < M) {
-          const int n = n0 + c0;
-          if (EPI == EPI_RESID) {
-            float* o = static_cast<float*>(out) + m * ldo + n;
-            const float* rs = resid + m * ldr + n;
+      constexpr int SLAB = BN / 2 >= 64 ? 64 : BN / 2;  // columns staged at a time
+      for (int c0 = part * (BN / 2); c0 < (part + 1) * (BN / 2); c0 += SLAB) {
+        // TMEM -> (acc + bias [, GELU]) -> warp-private staging, row = lane
 #pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-              const float4 r4 = *reinterpret_cast<const float4*>(rs + j);
-              const float4 b4 = *reinterpret_cast<const float4*>(bias + n + j);
-              float4 o4;
-              o4.x = r4.x + (v[j] + b4.x);
-              o4.y = r4.y + (v[j + 1] + b4.y);
-              o4.z = r4.z + (v[j + 2] + b4.z);
-              o4.w = r4.w + (v[j + 3] + b4.w);
-              *reinterpret_cast<float4*>(o + j) = o4;
-            }
-          } else {
-            uint32_t pk[8];
+        for (int q = 0; q < SLAB / 16; ++q) {
+          float v[16];
+          tc::tmem_ld16(trow + b * BN + c0 + 16 * q, v);
+          tc::tmem_wait_ld();
+          const int n = n0 + c0 + 16 * q;
 #pragma unroll
-            for (int j = 0; j < 16; j += 2) {
-              float a = v[j] + bias[n + j], c = v[j + 1] + bias[n + j + 1];
-              if (EPI == EPI_GELU) {
-                a = gelu_f(a);
-                c = gelu_f(c);
-              }
-              pk[j / 2] = tc::pack_bf16(a, c);
+          for (int j = 0; j < 16; ++j) {
+            float a = v[j] + bias[n + j];
+            if (EPI == EPI_GELU) a = gelu_f(a);
+            v[j] = a;
+          }
+          float4* d4 = reinterpret_cast<float4*>(stg + lane * TCW_STG_PITCH + 16 * q);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+        __syncwarp();
+        if (EPI == EPI_RESID) {
+          // SLAB fp32 per row, 16 B per lane
+          constexpr int LPR = SLAB / 4, RPP = 32 / LPR;
+#pragma unroll 4
+          for (int pass = 0; pass < 32 / RPP; ++pass) {
+            const int r = RPP * pass + lane / LPR, cc = (lane % LPR) * 4;
+            if (m0 + r < M) {
+              const float4 a = *reinterpret_cast<const float4*>(stg + r * TCW_STG_PITCH + cc);
+              const int64_t m = m0 + r;
+              const float4 rr = *reinterpret_cast<const float4*>(resid + m * ldr + n0 + c0 + cc);
+              *reinterpret_cast<float4*>(static_cast<float*>(out) + m * ldo + n0 + c0 + cc) =
+                  make_float4(rr.x + a.x, rr.y + a.y, rr.z + a.z, rr.w + a.w);
             }
-            uint4* o = reinterpret_cast<uint4*>(static_cast<bf16*>(out) + m * ldo + n);
-            o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        } else {
+          // SLAB bf16 per row, 16 B (8 values) per lane
+          constexpr int LPR = SLAB / 8, RPP = 32 / LPR;
+#pragma unroll 4
+          for (int pass = 0; pass < 32 / RPP; ++pass) {
+            const int r = RPP * pass + lane / LPR, cc = (lane % LPR) * 8;
+            if (m0 + r < M) {
+              const float4 a = *reinterpret_cast<const float4*>(stg + r * TCW_STG_PITCH + cc);
+              const float4 c = *reinterpret_cast<const float4*>(stg + r * TCW_STG_PITCH + cc + 4);
+              *reinterpret_cast<uint4*>(static_cast<bf16*>(out) + (m0 + r) * ldo + n0 + c0 + cc) =
+                  make_uint4(tc::pack_bf16(a.x, a.y), tc::pack_bf16(a.z, a.w),
+                             tc::pack_bf16(c.x, c.y), tc::pack_bf16(c.z, c.w));
+            }
           }
         }
+        __syncwarp();
       }
       tc::fence_before();
       __syncwarp();
