@@ -112,6 +112,8 @@ class _Common:
             f("load_checkpoint").argtypes = [C.c_char_p]
             f("measure_and_emit").argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                               C.c_uint64, C.c_double, C.c_char_p]
+            f("log_prob_grad").argtypes = [C.c_void_p, P_U8, C.c_int64, P_F64, C.c_double,
+                                           P_F64, P_F64]
         f("taps").argtypes = [C.c_void_p, C.c_void_p, P_U8, P_I64, P_I32, P_F32,
                               P_F64, P_I32]
 
@@ -192,6 +194,25 @@ class OracleModel:
             self.lib._f("model_destroy")(self.h)
         except Exception:
             pass
+
+    def log_prob_grad(self, configs, weights, vq_tau=1.0):
+        """d/dtheta sum_i w_i log P(s_i) on the reference's tape (build_log_prob +
+        weighted_sum + backward, proj/src/trainer.cpp:236-244): ([(name, grad)],
+        log-probs)."""
+        configs = np.ascontiguousarray(configs, np.uint8)
+        w = np.ascontiguousarray(weights, np.float64)
+        params = self.params()
+        total = sum(p.size for _, p in params)
+        g = np.zeros(total)
+        lp = np.zeros(configs.shape[0])
+        self.lib._check(self.lib._f("log_prob_grad")(
+            self.h, _p(configs, C.c_uint8), configs.shape[0], _p(w, C.c_double), vq_tau,
+            _p(g, C.c_double), _p(lp, C.c_double)))
+        out, off = [], 0
+        for name, p in params:
+            out.append((name, g[off:off + p.size].copy()))
+            off += p.size
+        return out, lp
 
     def save_checkpoint(self, path):
         self.lib._check(self.lib._f("save_checkpoint")(self.h, str(path).encode()))

@@ -34,6 +34,7 @@
 
 #include <Eigen/Dense>
 
+#include "vqnqs/autodiff.hpp"
 #include "vqnqs/bench.hpp"
 #include "vqnqs/checkpoint.hpp"
 #include "vqnqs/dedup.hpp"
@@ -267,6 +268,34 @@ int ref_measure_and_emit(void* mp, void* hp, int samples_per_batch, int batches,
     auto rep = measure_flops(*static_cast<VqTransformer*>(mp), *static_cast<HamiltonianModel*>(hp),
                              samples_per_batch, batches, rng, reference_per_site);
     emit_table({rep}, dir);
+  });
+}
+
+// The score-function gradient's backward (proj/src/trainer.cpp:213-246 with
+// the sample and its weights given): g = d/dtheta sum_i w_i log P(s_i)
+// through build_log_prob (proj/src/model.cpp:570-603) on the reference's own
+// tape (proj/src/autodiff.cpp), with its straight-through VQ surrogate.
+// grads: every parameter's gradient concatenated in parameters() order;
+// lp: the graph's log-probs.
+int ref_log_prob_grad(void* mp, const uint8_t* configs, int64_t B, const double* weights,
+                      double vq_tau, double* grads, double* lp) {
+  auto* m = static_cast<VqTransformer*>(mp);
+  return guarded([&] {
+    auto batch = unpack(configs, B, m->cfg.n_sites);
+    for (auto* p : m->parameters()) p->zero_grad();
+    m->cfg.vq_temperature = vq_tau;
+    m->cfg.vq_gumbel = false;
+    ad::Graph g;
+    auto ids = m->build_log_prob(g, batch, nullptr, nullptr);
+    const Tensor& lv = g.value(ids);
+    for (int64_t i = 0; i < B; ++i) lp[i] = lv.data[size_t(i)];
+    auto root = g.weighted_sum(ids, std::vector<double>(weights, weights + B));
+    g.backward(root);
+    size_t off = 0;
+    for (auto* p : m->parameters()) {
+      std::copy(p->grad.data.begin(), p->grad.data.end(), grads + off);
+      off += p->grad.data.size();
+    }
   });
 }
 
