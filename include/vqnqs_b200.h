@@ -119,6 +119,23 @@ int vqnqs_gpu_set_hamiltonian(vqnqs_handle* h, const int32_t* bonds, int nb,
 int vqnqs_gpu_sample(vqnqs_handle* h, int64_t count, uint64_t seed, uint64_t skip,
                      uint8_t* configs, double* log_probs);
 
+/* ---- the score-function gradient ---- */
+typedef struct vqnqs_grad_handle vqnqs_grad_handle;
+
+/* fp32 weights of the model on `device` for the backward pass. */
+int vqnqs_grad_create(const vqnqs_model_desc* d, const double* const* params, int n_params,
+                      int device, vqnqs_grad_handle** out);
+/* grads = d/dtheta sum_i weights[i] log P(configs[i]) — the backward of
+ * vmc_gradient (proj/src/trainer.cpp:236-244: build_log_prob, weighted_sum,
+ * backward; proj/src/autodiff.cpp) with the straight-through VQ surrogate at
+ * temperature vq_tau (Graph::vq_quantize, autodiff.cpp:536-655). grads: host,
+ * every parameter's gradient concatenated in parameters() order; log_probs:
+ * host [B], the dense log P of each configuration. Deterministic. */
+int vqnqs_grad_log_prob(vqnqs_grad_handle* h, const uint8_t* configs, int64_t B,
+                        const double* weights, double vq_tau, double* grads,
+                        double* log_probs);
+int vqnqs_grad_destroy(vqnqs_grad_handle* h);
+
 /* reuse = 1 (default): the compressed path. reuse = 0: the reference's
  * no-reuse regime (dense_local_energy, proj/src/bench.cpp:19-36 — every
  * connected configuration's full T-token forward, no shared prefixes, no

@@ -9,7 +9,8 @@ from .config import (CapabilityError, ConfigError, ModelConfig, NumericError, Sh
 
 _API = {"VqTransformer", "Parameter", "Lattice", "build_lattice", "HamiltonianModel",
         "zero_sz_samples", "Ledger", "LocalEnergyEngine", "local_energies",
-        "local_energy_batch", "VmcEstimate", "fill_stats", "param_shapes"}
+        "local_energy_batch", "VmcEstimate", "fill_stats", "param_shapes", "LogProbGradient",
+        "vmc_gradient"}
 
 
 def __getattr__(name):

@@ -378,3 +378,68 @@ def fill_stats(e_loc) -> VmcEstimate:
     mean = float(np.sum(e.real)) / k
     var = float(np.sum((e.real - mean) ** 2)) / (k - 1) if k > 1 else 0.0
     return VmcEstimate(mean, var, math.sqrt(var / k), e)
+
+
+# ---------------------------------------------------------------- gradient
+
+
+class LogProbGradient:
+    """d/dtheta sum_i w_i log P(s_i) on the GPU: the
+    backward of vmc_gradient (proj/src/trainer.cpp:236-244) through the dense
+    decoder with the straight-through VQ surrogate (autodiff.cpp:536-655)."""
+
+    def __init__(self, model: VqTransformer, device: int = 0):
+        self.model = model
+        self.cfg = model.cfg
+        desc = N.desc_of(model.cfg)
+        vals = [np.ascontiguousarray(p.value, np.float64).reshape(-1) for p in model.params]
+        arr = (N.P_F64 * len(vals))(*[N.ptr(v, C.c_double) for v in vals])
+        h = C.c_void_p()
+        N.check(N.lib().vqnqs_grad_create(C.byref(desc), arr, len(vals), device, C.byref(h)))
+        self._h = h
+        self._sizes = [int(p.value.size) for p in model.params]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().vqnqs_grad_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def grad(self, configs, weights, vq_tau: float = 1.0):
+        """([Parameter(name, grad)] in parameters() order, log P per sample)."""
+        cfgs = np.ascontiguousarray(configs, np.uint8)
+        w = np.ascontiguousarray(weights, np.float64)
+        if cfgs.ndim != 2 or cfgs.shape[1] != self.cfg.n_sites or w.shape != (cfgs.shape[0],):
+            raise ShapeError("configs [B x n_sites] and weights [B] expected")
+        g = np.zeros(sum(self._sizes))
+        lp = np.zeros(cfgs.shape[0])
+        N.check(N.lib().vqnqs_grad_log_prob(self._h, N.ptr(cfgs, C.c_uint8), cfgs.shape[0],
+                                            N.ptr(w, C.c_double), float(vq_tau),
+                                            N.ptr(g, C.c_double), N.ptr(lp, C.c_double)))
+        out, off = [], 0
+        for p, n in zip(self.model.params, self._sizes):
+            out.append(Parameter(p.name, g[off:off + n].reshape(p.value.shape)))
+            off += n
+        return out, lp
+
+
+def vmc_gradient(engine: LocalEnergyEngine, grad: LogProbGradient, k_samples: int, seed: int,
+                 vq_tau: float = 1.0, skip: int = 0):
+    """vmc_gradient (proj/src/trainer.cpp:213-246, phase network off, gumbel
+    off) on the GPU: K samples drawn with the model's sampler, local energies,
+    weights w_i = Re(E_i - mean E) / K, then the backward. Returns
+    ([Parameter(name, grad)], VmcEstimate)."""
+    if k_samples < 2:
+        raise ConfigError("k_samples must be >= 2")
+    configs, _ = engine.sample(k_samples, seed, skip=skip)
+    e, _ = engine.local_energies(configs)
+    est = fill_stats(e)
+    cmean = np.sum(e) / k_samples
+    wa = np.real(e - cmean) / k_samples
+    grads, _ = grad.grad(configs, wa, vq_tau)
+    return grads, est

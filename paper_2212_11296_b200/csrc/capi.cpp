@@ -12,6 +12,9 @@
 struct vqnqs_handle {
   vqb::Engine* eng;
 };
+struct vqnqs_grad_handle {
+  vqb::GradEngine* g;
+};
 
 namespace {
 thread_local std::string g_err;
@@ -111,6 +114,38 @@ int vqnqs_gpu_sample(vqnqs_handle* h, int64_t count, uint64_t seed, uint64_t ski
   return guarded([&] {
     if (!h || !configs || !log_probs) throw vqb::UsageError("null argument");
     h->eng->sample(count, seed, skip, configs, log_probs);
+  });
+}
+
+int vqnqs_grad_create(const vqnqs_model_desc* d, const double* const* params, int n_params,
+                      int device, vqnqs_grad_handle** out) {
+  return guarded([&] {
+    if (!d || !params || !out) throw vqb::UsageError("null argument");
+    auto* h = new vqnqs_grad_handle{nullptr};
+    try {
+      h->g = new vqb::GradEngine(*d, params, n_params, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int vqnqs_grad_log_prob(vqnqs_grad_handle* h, const uint8_t* configs, int64_t B,
+                        const double* weights, double vq_tau, double* grads, double* log_probs) {
+  return guarded([&] {
+    if (!h || !configs || !weights || !grads || !log_probs) throw vqb::UsageError("null argument");
+    h->g->log_prob_grad(configs, B, weights, vq_tau, grads, log_probs);
+  });
+}
+
+int vqnqs_grad_destroy(vqnqs_grad_handle* h) {
+  return guarded([&] {
+    if (h) {
+      delete h->g;
+      delete h;
+    }
   });
 }
 

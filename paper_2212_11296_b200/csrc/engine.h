@@ -60,6 +60,22 @@ void rng_uniforms(uint64_t seed, int64_t n, double* out);
 void ledger_add(const vqnqs_model_desc& c, int64_t K, const int64_t* U, int64_t* led);
 
 class EngineImpl;
+class GradImpl;
+
+// d/dtheta sum_i w_i log P(s_i) on the GPU
+// (proj/src/trainer.cpp:213-246 backward through build_log_prob,
+// proj/src/model.cpp:570-603, with the VQ surrogate of autodiff.cpp:536-655).
+class GradEngine {
+ public:
+  GradEngine(const vqnqs_model_desc& d, const double* const* params, int n_params, int device);
+  ~GradEngine();
+  // grads: parameters() order, concatenated (host); lp: log P per sample (host)
+  void log_prob_grad(const uint8_t* configs, int64_t B, const double* weights, double vq_tau,
+                     double* grads, double* lp);
+
+ private:
+  GradImpl* p_;
+};
 
 class Engine {
  public:
