@@ -294,6 +294,21 @@ def main():
                    "seconds": dt, "mean_log_prob": float(np.mean(lp_s)),
                    "method": "one position per step for all samples, per-block K/V cache"}
 
+    # the score-function gradient's backward (vmc_gradient):
+    # dense forward + backward of sum_i w_i log P(s_i) over 256 samples
+    gradient = None
+    if not args.no_sampler:
+        gengine = P.LogProbGradient(model, device=local)
+        nb_g = min(B, 256)
+        wts = np.linspace(-1.0, 1.0, nb_g)
+        gengine.grad(host_cfg[:8], wts[:8])
+        t0 = time.perf_counter()
+        gengine.grad(host_cfg[:nb_g], wts)
+        dt = time.perf_counter() - t0
+        gradient = {"value": nb_g * ws / dt, "unit": "samples/s", "samples_per_rank": nb_g,
+                    "seconds": dt, "precision": "fp32 (cuBLAS fp32 GEMMs)"}
+        gengine.close()
+
     # the reference's no-reuse regime (dense_local_energy,
     # proj/src/bench.cpp:19-36) on the same batch: the dedup saving in wall time
     dense = None
@@ -392,6 +407,7 @@ def main():
         "gpu_launches": int(launches_per_step * args.steps),
         "no_reuse": dense,
         "sampler": sampler,
+        "vmc_gradient": gradient,
         "clocks": clk,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
