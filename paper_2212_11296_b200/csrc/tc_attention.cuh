@@ -381,8 +381,12 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     bool live = false;
     int64_t myloc = 0;
     int kb_base = 0;
-    int nb = 0, nq = 0, wo_beg = 0;  // warp's live chunks: nb base + (nq - nb) own from wo_beg
-    int a = 0, own_lo = 0, own_cnt = 0;
+    // per-tile chunk slots (slot i = chunk part + 4i of the warp's live chunks:
+    // base chunks, then own chunks), packed once per tile:
+    //   sc_[i] = S column | P column << 9,  oc_[i] = (off + 512) | cnt << 10
+    //   (entry j of the chunk is live iff 0 <= off + j < cnt); sflags bit i:
+    //   slot live, bit 4 + i: every live row uses the whole chunk
+    uint32_t sc_[4] = {0, 0, 0, 0}, oc_[4] = {0, 0, 0, 0}, sflags = 0;
     float xn2 = 0.f, rr2 = 0.f;
     int nloc = 0;
     int j = 0, gi = 0;  // item it = (j, gi)
@@ -395,17 +399,32 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         nloc = reinterpret_cast<const int32_t*>(ti + 1544)[0];
         live = row < nloc;
         myloc = *reinterpret_cast<const int64_t*>(ti + 1536) + row;
-        a = reinterpret_cast<const int16_t*>(ti + 1024)[row];
-        own_lo = reinterpret_cast<const int16_t*>(ti + 1280)[row];
-        own_cnt = live ? row - own_lo + 1 : 0;
+        const int a = reinterpret_cast<const int16_t*>(ti + 1024)[row];
+        const int own_lo = reinterpret_cast<const int16_t*>(ti + 1280)[row];
+        const int own_cnt = live ? row - own_lo + 1 : 0;
         kb_base = kb_of(j);
         const int wb_end = (warp_max_i(a) + 15) & ~15;
         const int w_olo = warp_min_i(live ? own_lo : 1 << 20);
         const int w_ohi = warp_max_i(live ? row : -1);
-        wo_beg = w_olo >= 128 ? 128 : (w_olo & ~15);
+        const int wo_beg = w_olo >= 128 ? 128 : (w_olo & ~15);
         const int wo_end = w_ohi < 0 ? 0 : ((w_ohi + 16) & ~15);
-        nb = wb_end >> 4;
-        nq = nb + max(0, (wo_end - wo_beg) >> 4);
+        const int nb = wb_end >> 4;
+        const int nq = nb + max(0, (wo_end - wo_beg) >> 4);
+        sflags = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int q = part + 4 * i;
+          const bool isb = q < nb;
+          const int c0 = isb ? 16 * q : wo_beg + 16 * (q - nb);
+          const int off = isb ? c0 : c0 - own_lo;
+          const int cnt = isb ? a : own_cnt;
+          sc_[i] = (uint32_t)((isb ? TS_BASE : TS_OWN) + c0) |
+                   ((uint32_t)((isb ? c0 : kb_base + c0) >> 1) << 9);
+          oc_[i] = (uint32_t)(off + 512) | ((uint32_t)cnt << 10);
+          const bool full = __all_sync(0xffffffffu, !live || (off >= 0 && off + 16 <= cnt));
+          sflags |= (q < nq ? 1u : 0u) << i;
+          sflags |= (full ? 1u : 0u) << (4 + i);
+        }
         xn2 = 0.f;
         rr2 = 0.f;
         // P columns no warp writes this tile must read as zero
@@ -429,16 +448,12 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         uint32_t pcol[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int q = part + 4 * i;
-          sl[i] = q < nq;
-          const bool isb = q < nb;
-          const int c0 = isb ? 16 * q : wo_beg + 16 * (q - nb);
-          off[i] = isb ? c0 : c0 - own_lo;  // entry j is live iff 0 <= off + j < cnt
-          cnt[i] = isb ? a : own_cnt;
-          pcol[i] = (uint32_t)((isb ? c0 : kb_base + c0) >> 1);
-          // chunk live in full for every live row of the warp: no masking
-          full[i] = __all_sync(0xffffffffu, !live || (off[i] >= 0 && off[i] + 16 <= cnt[i]));
-          if (sl[i]) tc::tmem_ld16(trow + (isb ? TS_BASE : TS_OWN) + c0, v[i]);
+          sl[i] = (sflags >> i) & 1u;
+          full[i] = (sflags >> (4 + i)) & 1u;
+          off[i] = (int)(oc_[i] & 1023u) - 512;
+          cnt[i] = (int)(oc_[i] >> 10);
+          pcol[i] = sc_[i] >> 9;
+          if (sl[i]) tc::tmem_ld16(trow + (sc_[i] & 511u), v[i]);
         }
         tc::tmem_wait_ld();
         tc::fence_before();
