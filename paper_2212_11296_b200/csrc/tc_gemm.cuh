@@ -1,15 +1,8 @@
 // tcgen05 GEMM for the per-location linear layers on unique rows
-// (QKV, Wo, W1, W2; proj/src/dedup.cpp:220-267): C = A . W + b with fused
-// epilogues (bf16 store, GELU, fp32 residual add). A rows may be gathered
-// (the continuation's codebook rows). A is bf16 [M x K] row-major, W is
-// supplied transposed (W^T [N x K], K-major) so both UMMA operands are K-major.
-//
-// One CTA (4 warps) owns a 128 x BN output tile at a time (persistent over
-// tiles; M read from device memory). All threads stage operands with
-// cp.async into a STAGES-deep ring of SW128 tiles; thread 0 issues
-// tcgen05.mma (M=128, N=BN, K=16) into a BN-column TMEM accumulator and
-// commits each stage to an mbarrier that gates the stage's reuse; after the
-// last K block the four warps drain TMEM (32 lanes each) through the epilogue.
+// (QKV, W1, W2 and the per-code Wo tables; proj/src/dedup.cpp:220-267):
+// C = A . W + b with fused epilogues (bf16 store, GELU, fp32 residual add).
+// A is bf16 [M x K] row-major, W is supplied transposed (W^T [N x K],
+// K-major) so both UMMA operands are K-major.
 #pragma once
 
 #include "common.cuh"
@@ -18,155 +11,7 @@
 
 namespace vqb {
 
-constexpr int TCG_STAGES = 3;
-constexpr int TCG_BK = 64;
-
-template <int BN>
-constexpr size_t tcg_smem_bytes() {
-  return size_t(TCG_STAGES) * (128 * 128 + BN * 128) + 1024 /*align*/ + 256 /*barriers*/;
-}
-
-template <int BN, int EPI, bool GATHER>
-__global__ void __launch_bounds__(128, 1) k_tc_gemm(
-    const int64_t* __restrict__ Mp, int N, int K, const bf16* __restrict__ A, int lda,
-    const int32_t* __restrict__ gA, const bf16* __restrict__ WT, const float* __restrict__ bias,
-    void* __restrict__ out, int ldo, const float* __restrict__ resid, int ldr,
-    const int64_t* __restrict__ gR) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  constexpr uint32_t A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + TCG_STAGES * STAGE);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + TCG_STAGES);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t M = *Mp;
-  const int64_t tilesM = (M + 127) / 128;
-  const int tilesN = N / BN;
-  const int KB = K / TCG_BK;
-  if (tid == 0) {
-    for (int s = 0; s < TCG_STAGES; ++s) tc::mbar_init(&mbar[s], 1);
-    tc::mbar_fence_init();
-  }
-  if (warp == 0) tc::tmem_alloc(tmem_slot, BN < 32 ? 32 : BN);
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t sbase = tc::smem_u32(smem);
-  constexpr uint32_t idesc = tc::make_idesc_bf16(128, BN);
-  uint32_t g = 0;  // global k-block counter (stage ring position)
-
-  for (int64_t tile = blockIdx.x; tile < tilesM * tilesN; tile += gridDim.x) {
-    const int64_t m0 = (tile / tilesN) * 128;
-    const int n0 = int(tile % tilesN) * BN;
-    auto load = [&](int kb, uint32_t gg) {
-      const uint32_t s = gg % TCG_STAGES;
-      const uint32_t sa = sbase + s * STAGE, sb = sa + A_BYTES;
-      const int k0 = kb * TCG_BK;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {  // A: 128 rows x 8 chunks
-        const int e = tid + i * 128;
-        const int r = e >> 3, c = e & 7;
-        const int64_t m = m0 + r;
-        const bool ok = m < M;
-        const int64_t ar = ok ? (GATHER ? (int64_t)gA[m] : m) : 0;
-        tc::cp_async16_zfill(sa + tc::sw128_chunk(r, c), A + ar * lda + k0 + c * 8, ok);
-      }
-#pragma unroll
-      for (int i = 0; i < BN / 16; ++i) {  // B: BN rows x 8 chunks
-        const int e = tid + i * 128;
-        const int r = e >> 3, c = e & 7;
-        tc::cp_async16(sb + tc::sw128_chunk(r, c), WT + (int64_t)(n0 + r) * K + k0 + c * 8);
-      }
-    };
-    // prologue
-    for (int p = 0; p < TCG_STAGES - 1; ++p) {
-      if (p < KB) {
-        const uint32_t gg = g + p;
-        if (gg >= TCG_STAGES) tc::mbar_wait(&mbar[gg % TCG_STAGES], ((gg / TCG_STAGES) - 1) & 1);
-        load(p, gg);
-      }
-      tc::cp_async_commit();
-    }
-    for (int kb = 0; kb < KB; ++kb) {
-      const int pf = kb + TCG_STAGES - 1;
-      if (pf < KB) {
-        const uint32_t gg = g + pf;
-        if (gg >= TCG_STAGES) tc::mbar_wait(&mbar[gg % TCG_STAGES], ((gg / TCG_STAGES) - 1) & 1);
-        load(pf, gg);
-      }
-      tc::cp_async_commit();
-      tc::cp_async_wait<TCG_STAGES - 1>();
-      tc::fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
-        tc::fence_after();
-        const uint32_t s = (g + kb) % TCG_STAGES;
-        const uint32_t sa = sbase + s * STAGE, sb = sa + A_BYTES;
-#pragma unroll
-        for (int k = 0; k < TCG_BK / 16; ++k)
-          tc::mma_bf16(tmem, tc::make_desc_sw128(sa + k * 32), tc::make_desc_sw128(sb + k * 32),
-                       idesc, (kb | k) != 0);
-        tc::mma_commit(&mbar[s]);
-      }
-    }
-    // wait for the tile's last MMA
-    {
-      const uint32_t gl = g + KB - 1;
-      tc::mbar_wait(&mbar[gl % TCG_STAGES], (gl / TCG_STAGES) & 1);
-    }
-    g += KB;
-    tc::fence_after();
-    // epilogue: warp w drains TMEM lanes [32w, 32w+32) = tile rows
-    const int64_t m = m0 + warp * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      tc::tmem_ld16(trow + c0, v);
-      tc::tmem_wait_ld();
-      if (m < M) {
-        const int n = n0 + c0;
-        if (EPI == EPI_RESID) {
-          const int64_t rr = gR ? gR[m] : m;
-          float* o = static_cast<float*>(out) + m * ldo + n;
-          const float* rs = resid + rr * ldr + n;
-#pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            const float4 r4 = *reinterpret_cast<const float4*>(rs + j);
-            const float4 b4 = *reinterpret_cast<const float4*>(bias + n + j);
-            float4 o4;
-            o4.x = r4.x + (v[j] + b4.x);
-            o4.y = r4.y + (v[j + 1] + b4.y);
-            o4.z = r4.z + (v[j + 2] + b4.z);
-            o4.w = r4.w + (v[j + 3] + b4.w);
-            *reinterpret_cast<float4*>(o + j) = o4;
-          }
-        } else {
-          uint32_t pk[8];
-#pragma unroll
-          for (int j = 0; j < 16; j += 2) {
-            float a = v[j] + bias[n + j], b = v[j + 1] + bias[n + j + 1];
-            if (EPI == EPI_GELU) {
-              a = gelu_f(a);
-              b = gelu_f(b);
-            }
-            pk[j / 2] = tc::pack_bf16(a, b);
-          }
-          uint4* o = reinterpret_cast<uint4*>(static_cast<bf16*>(out) + m * ldo + n);
-          o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        }
-      }
-    }
-    tc::fence_before();
-    __syncthreads();
-  }
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, BN < 32 ? 32 : BN);
-}
-
-// Warp-specialised persistent variant for contiguous A (QKV, W1, W2 and the
-// per-code table): warp 0 issues TMA for A [128 x 64] and W^T [BN x 64]
+// Warp-specialised persistent kernel: warp 0 issues TMA for A [128 x 64] and W^T [BN x 64]
 // K-blocks into a 4-stage ring, warp 1 issues tcgen05.mma into one of two
 // BN-column TMEM accumulators, warps 2-9 (two warpgroups, BN/2 columns each)
 // drain the other accumulator through the fused epilogue, so loads, MMAs and

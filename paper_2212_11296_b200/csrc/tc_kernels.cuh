@@ -18,47 +18,6 @@ inline bool tc_gemm_ok(int prec, int N, int K) {
 }
 inline bool tc_vq_ok(int prec, int d, int Q) { return prec == 1 && d % 64 == 0 && Q % 256 == 0; }
 
-template <int BN, int EPI, bool G>
-inline void launch_tc_gemm_inst(const int64_t* Mp, int64_t Mcap, int N, int K, const bf16* A,
-                                int lda, const int32_t* gA, const bf16* WT, const float* bias,
-                                void* out, int ldo, const float* resid, int ldr,
-                                const int64_t* gR, cudaStream_t st, int sms) {
-  const size_t smem = tcg_smem_bytes<BN>();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tc_gemm<BN, EPI, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    attr = true;
-  }
-  const int64_t tiles = ((Mcap + 127) / 128) * (N / BN);
-  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
-  k_tc_gemm<BN, EPI, G><<<grid, 128, smem, st>>>(Mp, N, K, A, lda, gA, WT, bias, out, ldo, resid,
-                                                 ldr, gR);
-}
-
-template <int BN>
-inline void launch_tc_gemm_bn(const int64_t* Mp, int64_t Mcap, int N, int K, const bf16* A, int lda,
-                              const int32_t* gA, const bf16* WT, const float* bias, void* out,
-                              int ldo, int epi, const float* resid, int ldr, const int64_t* gR,
-                              cudaStream_t st, int sms) {
-  if (gA) {
-    if (epi == EPI_RESID)
-      launch_tc_gemm_inst<BN, EPI_RESID, true>(Mp, Mcap, N, K, A, lda, gA, WT, bias, out, ldo,
-                                               resid, ldr, gR, st, sms);
-    else
-      throw std::runtime_error("tc_gemm: gathered A only with the residual epilogue");
-  } else if (epi == EPI_STORE) {
-    launch_tc_gemm_inst<BN, EPI_STORE, false>(Mp, Mcap, N, K, A, lda, gA, WT, bias, out, ldo,
-                                              resid, ldr, gR, st, sms);
-  } else if (epi == EPI_GELU) {
-    launch_tc_gemm_inst<BN, EPI_GELU, false>(Mp, Mcap, N, K, A, lda, gA, WT, bias, out, ldo,
-                                             resid, ldr, gR, st, sms);
-  } else {
-    launch_tc_gemm_inst<BN, EPI_RESID, false>(Mp, Mcap, N, K, A, lda, gA, WT, bias, out, ldo,
-                                              resid, ldr, gR, st, sms);
-  }
-}
-
 template <int BN, int EPI>
 inline void launch_tc_gemm_ws(const int64_t* Mp, int64_t Mcap, int N, int K, const bf16* A,
                               int lda, const bf16* WT, const float* bias, void* out, int ldo,
@@ -99,28 +58,14 @@ inline void tc_gemm(const int64_t* Mp, int64_t Mcap, int N, int K, const void* A
                     int sms) {
   const bf16* a = static_cast<const bf16*>(A);
   const bf16* w = static_cast<const bf16*>(WT);
-  if (!gA && !gR && !getenv("VQNQS_GEMM_V1")) {
-    // warp-specialised TMA path (contiguous A rows, identity residual rows)
-    if (N % 256 == 0)
-      launch_tc_gemm_ws_bn<256>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, epi, resid, ldr, st,
-                                sms);
-    else if (N % 128 == 0)
-      launch_tc_gemm_ws_bn<128>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, epi, resid, ldr, st,
-                                sms);
-    else
-      launch_tc_gemm_ws_bn<64>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, epi, resid, ldr, st,
-                               sms);
-    return;
-  }
+  if (gA || gR) throw std::runtime_error("tc_gemm: gathered operands are not supported");
+  // warp-specialised TMA path (contiguous A rows, identity residual rows)
   if (N % 256 == 0)
-    launch_tc_gemm_bn<256>(Mp, Mcap, N, K, a, lda, gA, w, bias, out, ldo, epi, resid, ldr, gR, st,
-                           sms);
+    launch_tc_gemm_ws_bn<256>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, epi, resid, ldr, st, sms);
   else if (N % 128 == 0)
-    launch_tc_gemm_bn<128>(Mp, Mcap, N, K, a, lda, gA, w, bias, out, ldo, epi, resid, ldr, gR, st,
-                           sms);
+    launch_tc_gemm_ws_bn<128>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, epi, resid, ldr, st, sms);
   else
-    launch_tc_gemm_bn<64>(Mp, Mcap, N, K, a, lda, gA, w, bias, out, ldo, epi, resid, ldr, gR, st,
-                          sms);
+    launch_tc_gemm_ws_bn<64>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, epi, resid, ldr, st, sms);
 }
 
 // bf16 copy and |x|^2, |x - bf16(x)|^2 of fp32 attention rows, for the VQ
