@@ -35,10 +35,16 @@ constexpr int TCV_A_BYTES = 128 * 128;
 constexpr int TCV_B_BYTES = TCV_NCH * 128;
 constexpr int TCV_STAGE_BYTES = 2 * TCV_A_BYTES + TCV_B_BYTES;
 constexpr int TCV_CAND = 8;
-constexpr int TCV_THREADS = 320;  // producer warp, MMA warp, 8 epilogue warps
+// producer warp, MMA warp, 16 epilogue warps: four per TMEM lane quadrant,
+// each taking 64 of an accumulator's 256 columns (enough warps that the
+// epilogue drains one accumulator faster than the MMAs fill the other)
+constexpr int TCV_EPI_PARTS = 4;
+constexpr int TCV_THREADS = 64 + 32 * 4 * TCV_EPI_PARTS;
+constexpr int TCV_QCAND = TCV_EPI_PARTS * TCV_CAND;  // queued survivors per row
 
 inline size_t tcv_smem_bytes(int Q) {
-  return 1024 + size_t(TCV_STAGES) * TCV_STAGE_BYTES + 256 + size_t(Q) * 4 + 2 * 128 * 12 + 64;
+  return 1024 + size_t(TCV_STAGES) * TCV_STAGE_BYTES + 256 + size_t(Q) * 4 +
+         size_t(TCV_EPI_PARTS) * 128 * 12 + 64;
 }
 
 __device__ __forceinline__ double vq_exact_d2(const bf16* __restrict__ xh,
@@ -90,8 +96,8 @@ __device__ __noinline__ void cand_add(Cands& C, float dt, int j, float thr) {
   }
 }
 
-__device__ __forceinline__ void epi_bar() {  // the 256 epilogue threads
-  asm volatile("bar.sync 1, 256;" ::: "memory");
+__device__ __forceinline__ void epi_bar() {  // the epilogue threads
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * 4 * TCV_EPI_PARTS) : "memory");
 }
 
 __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
@@ -111,9 +117,9 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float* wn2 = reinterpret_cast<float*>(tail + 256);
-  float* red_min = wn2 + Q;                                 // [2][128]
-  int* red_cnt = reinterpret_cast<int*>(red_min + 256);     // [2][128]
-  int* red_jf = red_cnt + 256;                              // [2][128]
+  float* red_min = wn2 + Q;                                              // [parts][128]
+  int* red_cnt = reinterpret_cast<int*>(red_min + TCV_EPI_PARTS * 128);  // [parts][128]
+  int* red_jf = red_cnt + TCV_EPI_PARTS * 128;                           // [parts][128]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t M = *Mp;
   const int KB = d / 64;
@@ -126,7 +132,7 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&acc_full[b], 1);
-      tc::mbar_init(&acc_empty[b], 8);
+      tc::mbar_init(&acc_empty[b], 4 * TCV_EPI_PARTS);
     }
     tc::mbar_fence_init();
     tc::prefetch_tmap(&tmA);
@@ -189,9 +195,10 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
       }
     }
   } else {
-    // ---------------- epilogue: 8 warps, warp w drains TMEM lanes 32 (w % 4)
+    // ---------------- epilogue: warp w drains TMEM lanes 32 (w % 4)
     const int row = (warp & 3) * 32 + lane;
-    const int part = (warp - 2) >> 2;  // 0 or 1: columns [128 part, 128 part + 128)
+    const int part = (warp - 2) >> 2;  // columns [PW part, PW part + PW) of a chunk
+    constexpr int PW = TCV_NCH / TCV_EPI_PARTS;
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     uint32_t acc = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -211,7 +218,7 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
         const uint32_t b = acc & 1;
         tc::mbar_wait(&acc_full[b], (acc >> 1) & 1);
         tc::fence_after();
-        for (int c0 = part * 128; c0 < part * 128 + 128; c0 += 32) {
+        for (int c0 = part * PW; c0 < part * PW + PW; c0 += 32) {
           float v[32];
           tc::tmem_ld32(trow + b * TCV_NCH + c0, v);
           tc::tmem_wait_ld();
@@ -237,7 +244,9 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
       // ---- merge the two warpgroups' survivors for this row
       red_min[part * 128 + row] = run_min;
       epi_bar();
-      const float gmin = fminf(red_min[row], red_min[128 + row]);
+      float gmin = red_min[row];
+#pragma unroll
+      for (int q = 1; q < TCV_EPI_PARTS; ++q) gmin = fminf(gmin, red_min[q * 128 + row]);
       int mine = 0, jfirst = 0x7fffffff;
 #pragma unroll 1
       for (int i = 0; i < C.n; ++i)
@@ -248,18 +257,25 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
       red_cnt[part * 128 + row] = C.overflow ? 1000 : mine;
       red_jf[part * 128 + row] = jfirst;
       epi_bar();
-      const int total = red_cnt[row] + red_cnt[128 + row];
+      int total = 0, before = 0, jf = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < TCV_EPI_PARTS; ++q) {
+        const int cq = red_cnt[q * 128 + row];
+        if (q < part) before += cq;
+        total += cq;
+        jf = min(jf, red_jf[q * 128 + row]);
+      }
       if (live) {
         if (total == 1) {
-          if (part == 0) code[my] = min(red_jf[row], red_jf[128 + row]);
+          if (part == 0) code[my] = jf;
         } else {
-          // queue the row: warpgroup 0's survivors first, then warpgroup 1's
+          // queue the row: the parts' survivors in part order
           const bool over = total >= 1000;
           if (!over) {
-            int w = part == 0 ? 0 : red_cnt[row];
+            int w = before;
 #pragma unroll 1
             for (int i = 0; i < C.n; ++i)
-              if (C.d[i] <= gmin + w2) cand[my * (2 * TCV_CAND) + w++] = C.j[i];
+              if (C.d[i] <= gmin + w2) cand[my * TCV_QCAND + w++] = C.j[i];
           }
           if (part == 0) {
             ncand[my] = over ? -1 : total;
@@ -295,7 +311,7 @@ __global__ void __launch_bounds__(256) k_vq_rescore(
     int jb = 0x7fffffff;
     if (n >= 0) {
       if (lane < n) {
-        jb = cand[row * (2 * TCV_CAND) + lane];
+        jb = cand[row * TCV_QCAND + lane];
         best = vq_exact_d2(xhr, xlr, cb32 + (int64_t)jb * d, d);
       }
       done += n;
@@ -335,7 +351,7 @@ struct VqScratch {
     if (rows <= cap && qcount) return;
     release();
     cap = rows + rows / 4 + 1024;
-    if (cudaMalloc(&cand, cap * 2 * TCV_CAND * sizeof(int32_t)) != cudaSuccess ||
+    if (cudaMalloc(&cand, cap * TCV_QCAND * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&ncand, cap * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&qrows, cap * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&qcount, sizeof(uint32_t)) != cudaSuccess)
