@@ -170,14 +170,29 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
     if (lane == 0) {
       constexpr uint32_t idesc = tc::make_idesc_bf16(128, TCV_NCH);
       uint32_t it = 0, acc = 0;
+#ifdef VQNQS_VQ_TRACE  // developer instrumentation: where the MMA warp waits
+      long long w_acc = 0, w_full = 0, t_all = clock64();
+#endif
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         for (int c = 0; c < NCH; ++c, ++acc) {
           const uint32_t b = acc & 1;
+#ifdef VQNQS_VQ_TRACE
+          long long t0 = clock64();
+#endif
           if (acc >= 2) tc::mbar_wait(&acc_empty[b], ((acc >> 1) - 1) & 1);
+#ifdef VQNQS_VQ_TRACE
+          w_acc += clock64() - t0;
+#endif
           tc::fence_after();
           for (int kb = 0; kb < KB; ++kb, ++it) {
             const uint32_t s = it % TCV_STAGES;
+#ifdef VQNQS_VQ_TRACE
+            long long t1 = clock64();
+#endif
             tc::mbar_wait(&full[s], (it / TCV_STAGES) & 1);
+#ifdef VQNQS_VQ_TRACE
+            w_full += clock64() - t1;
+#endif
             tc::fence_after();
             const uint32_t sa = sbase + s * TCV_STAGE_BYTES;
 #pragma unroll
@@ -193,6 +208,11 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
           tc::mma_commit(&acc_full[b]);
         }
       }
+#ifdef VQNQS_VQ_TRACE
+      if (blockIdx.x < 3)
+        printf("VQTR b%d total %lld wait_acc_empty %lld wait_full %lld stages %u\n", blockIdx.x,
+               clock64() - t_all, w_acc, w_full, it);
+#endif
     }
   } else {
     // ---------------- epilogue: warp w drains TMEM lanes 32 (w % 4)
