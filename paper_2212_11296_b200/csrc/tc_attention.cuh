@@ -152,7 +152,7 @@ struct AttnSmem {
     info = 2 * stage;
     out = info + 4 * TINFO_BYTES;
     bar = out + 2 * 128 * ATT_OPITCH;
-    total = bar + 64;  // 6 mbarriers, TMEM base
+    total = bar + 80;  // 8 mbarriers, TMEM base
   }
 };
 
@@ -199,8 +199,9 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   uint64_t* s_free = mbar + 1;
   uint64_t* p_full = mbar + 2;
   uint64_t* pv_done = mbar + 3;
-  uint64_t* st_full = mbar + 4;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 6);
+  uint64_t* st_full = mbar + 4;     // [2]
+  uint64_t* stage_free = mbar + 6;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 8);
   // exchange buffers alternate by head: a fast warp may publish head h+1
   // before a slow one of its quadrant has read head h
   __shared__ float2 red[2][4][128];  // (local max, local sum)
@@ -222,8 +223,10 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     tc::mbar_init(s_free, TCA_SOFTMAX_WARPS);
     tc::mbar_init(p_full, TCA_SOFTMAX_WARPS);
     tc::mbar_init(pv_done, 1);
-    tc::mbar_init(&st_full[0], TCA_SOFTMAX_WARPS);
-    tc::mbar_init(&st_full[1], TCA_SOFTMAX_WARPS);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&st_full[i], 3);  // the three producer warps
+      tc::mbar_init(&stage_free[i], 1);
+    }
     tc::mbar_fence_init();
   }
   if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
@@ -305,12 +308,69 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         ph_p ^= 1;
         tc::fence_after();
         issue_pv(it, hh, kb_cur);
+        if (hh == hpg - 1) tc::mma_commit(&stage_free[it & 1]);  // item it's operands read
         if (it2 >= nit) break;
         it = it2;
         hh = hh2;
         j = j2;
         gi = gi2;
         kb_cur = kb_next;
+      }
+    }
+    if (warp > TCA_SOFTMAX_WARPS && nit > 0) {
+      // ================= producer warps: cp.async staging of every item into
+      // its stage once the item two back has released it, tile tables one
+      // tile ahead; three warps, 96 threads
+      const int ptid = tid - 32 * (TCA_SOFTMAX_WARPS + 1);
+      auto pbar = [&]() { asm volatile("bar.sync 6, 96;" ::: "memory"); };
+      auto fetch_info = [&](int j) {
+        if (j < my_tiles)
+          for (int c = ptid; c < TINFO_BYTES / 16; c += 96) {
+            const uint8_t* src = tinfo + (int64_t)(blockIdx.x + j * gridDim.x) * TINFO_BYTES;
+            tc::cp_async16(sb + L.info + (uint32_t)((j & 3) * TINFO_BYTES) + c * 16, src + c * 16);
+          }
+      };
+      fetch_info(0);
+      fetch_info(1);
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      pbar();
+      int j = 0, gi = 0;
+      for (int it = 0; it < nit; ++it) {
+        if (it >= 2) tc::mbar_wait(&stage_free[it & 1], ((it - 2) >> 1) & 1);
+        if (gi == 0 && j >= 1) fetch_info(j + 1);
+        const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
+        const int32_t* rq = reinterpret_cast<const int32_t*>(slot(j));
+        const int32_t* rb = rq + 128;
+        for (int e = ptid; e < 128 * 8; e += 96) {
+          const int r = e >> 3, c = e & 7;
+          const int64_t off = (int64_t)rq[r] * ld;
+          const bool ok = off >= 0;
+          const bf16* src = qkv + (ok ? off : 0) + gi * 64 + c * 8;
+          const uint32_t o = tc::sw128_chunk(r, c);
+          tc::cp_async16_zfill(st + L.q + o, src, ok);
+          tc::cp_async16_zfill(st + L.kown + o, src + d, ok);
+          tc::cp_async16_zfill(st + L.vown + o, src + 2 * d, ok);
+        }
+        for (int e = ptid; e < 64 * KBb * 8; e += 96) {
+          const int t = e >> 3, c = e & 7;
+          const int64_t off = t < 128 ? (int64_t)rb[t] * ld : -1;
+          const bool ok = off >= 0;
+          const bf16* src = qkv + (ok ? off : 0) + d + gi * 64 + c * 8;
+          const uint32_t o = tc::sw128_chunk(t, c);
+          tc::cp_async16_zfill(st + L.kbase + o, src, ok);
+          tc::cp_async16_zfill(st + L.vbase + o, src + d, ok);
+        }
+        tc::cp_async_commit();
+        tc::cp_async_wait<0>();
+        tc::fence_proxy_async();
+        pbar();  // every producer thread's copies (and the next table) landed
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&st_full[it & 1]));
+        if (++gi == G) {
+          gi = 0;
+          ++j;
+        }
       }
     }
   } else {
@@ -326,57 +386,6 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     };
     uint32_t ph_s = 0, ph_o = 0, hc = 0;
     ATR_DECL
-    // async copy of tile j's table into its slot (part of the caller's group)
-    auto fetch_info = [&](int j) {
-      if (j < my_tiles && tid < TINFO_BYTES / 16) {
-        const uint8_t* src = tinfo + (int64_t)(blockIdx.x + j * gridDim.x) * TINFO_BYTES;
-        tc::cp_async16(sb + L.info + (uint32_t)((j & 3) * TINFO_BYTES) + tid * 16, src + tid * 16);
-      }
-    };
-    // stage the operands of item `it` = (j, gi) (cp.async, zero-filled tails);
-    // the first item of tile j >= 1 also fetches tile j+1's table (tables 0
-    // and 1 are fetched up front)
-    auto prefetch = [&](int it, int j, int gi) {
-      if (it >= nit) return;
-      if (gi == 0 && j >= 1) fetch_info(j + 1);
-      const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
-      const int32_t* rq = reinterpret_cast<const int32_t*>(slot(j));
-      const int32_t* rb = rq + 128;
-      for (int e = tid; e < 128 * 8; e += 512) {
-        const int r = e >> 3, c = e & 7;
-        const int64_t off = (int64_t)rq[r] * ld;
-        const bool ok = off >= 0;
-        const bf16* src = qkv + (ok ? off : 0) + gi * 64 + c * 8;
-        const uint32_t o = tc::sw128_chunk(r, c);
-        tc::cp_async16_zfill(st + L.q + o, src, ok);
-        tc::cp_async16_zfill(st + L.kown + o, src + d, ok);
-        tc::cp_async16_zfill(st + L.vown + o, src + 2 * d, ok);
-      }
-      for (int e = tid; e < 64 * KBb * 8; e += 512) {
-        const int t = e >> 3, c = e & 7;
-        const int64_t off = t < 128 ? (int64_t)rb[t] * ld : -1;
-        const bool ok = off >= 0;
-        const bf16* src = qkv + (ok ? off : 0) + d + gi * 64 + c * 8;
-        const uint32_t o = tc::sw128_chunk(t, c);
-        tc::cp_async16_zfill(st + L.kbase + o, src, ok);
-        tc::cp_async16_zfill(st + L.vbase + o, src + d, ok);
-      }
-      tc::cp_async_commit();
-    };
-
-    if (nit > 0) {
-      fetch_info(0);
-      fetch_info(1);
-      tc::cp_async_commit();
-      tc::cp_async_wait<0>();
-      asm volatile("bar.sync 5, 512;" ::: "memory");  // tables 0, 1 visible to every warp
-      prefetch(0, 0, 0);
-      prefetch(1, G == 1 ? 1 : 0, G == 1 ? 0 : 1);
-      tc::cp_async_wait<1>();
-      tc::fence_proxy_async();
-      arrive(&st_full[0]);
-    }
-
     // per-tile thread state
     bool live = false;
     int64_t myloc = 0;
@@ -525,13 +534,6 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         arrive(p_full);  // O_h = P_base V_base + P_own V_own, issued by the MMA warp
         ATR(7)
       }
-      // ---- the next item's operands: landed -> signal the MMA warp, whose
-      // first score MMA for it then overlaps this item's drain
-      if (it + 1 < nit) {
-        tc::cp_async_wait<0>();
-        tc::fence_proxy_async();
-        arrive(&st_full[(it + 1) & 1]);
-      }
       ATR(8)
       tc::mbar_wait(pv_done, ph_o);  // the item's last value MMA
       ph_o ^= 1;
@@ -595,8 +597,6 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           rr2_out[myloc] = ((nrm[1][0][row] + nrm[1][1][row]) + nrm[1][2][row]) + nrm[1][3][row];
         }
       }
-      // into this item's stage: every MMA reading it has completed
-      prefetch(it + 2, g1 + 1 == G ? j1 + 1 : j1, g1 + 1 == G ? 0 : g1 + 1);
       ATR(11)
       j = j1;
       gi = g1;
