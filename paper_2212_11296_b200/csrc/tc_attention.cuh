@@ -150,9 +150,9 @@ struct AttnSmem {
     vbase = kbase + 64 * KBb * 128;
     stage = vbase + 64 * KBb * 128;
     info = 2 * stage;
-    out = info + 4 * TINFO_BYTES;
+    out = info + 8 * TINFO_BYTES;
     bar = out + 2 * 128 * ATT_OPITCH;
-    total = bar + 80;  // 8 mbarriers, TMEM base
+    total = bar + 160;  // 18 mbarriers, TMEM base
   }
 };
 
@@ -178,12 +178,24 @@ __device__ __forceinline__ float ex2_approx(float x) {
 //   s_free   (16 warp arrivals) every warp holds S(g) in registers
 //   p_full   (16 warp arrivals) P(g) written to TMEM
 //   pv_done  (MMA commit)      O += P(g) V done, P free
-//   st_full[2] (16 warp arrivals) the item's cp.async operands landed
-// The MMA warp sits in a fifth warpgroup that hands its registers to the
-// softmax warpgroups (setmaxnreg within the launch allocation 640 x 96:
-// 4 x 128 x 112 + 128 x 32).
+//   st_full[2]   (3 producer warps) the item's cp.async operands landed
+//   stage_free[2] (MMA commit)     every MMA of the item done (operands free,
+//                                   its O complete)
+//   o_empty[2]   (4 drain warps)   the item's O buffer drained
+//   info_ready[8] (3 producer warps) a tile table landed
+// Warpgroups: four softmax warpgroups; two drain warpgroups (warp 16 + 4h + q
+// drains half h of row quadrant q's O, double-buffered by item in TMEM, into
+// xh / xl and the row norms, so no softmax warp waits for an item's last
+// value MMA); and the MMA warpgroup (warp 24 issues every tcgen05.mma, warps
+// 25-27 stage the operands with cp.async). setmaxnreg redistributes the
+// 896 x 72 launch registers: softmax 96, drain 40, MMA / producers 32.
 constexpr int TCA_SOFTMAX_WARPS = 16;
-constexpr int TCA_THREADS = 32 * (TCA_SOFTMAX_WARPS + 4);
+constexpr int TCA_DRAIN_WARP0 = 16;
+constexpr int TCA_DRAIN_WARPS = 8;  // two per row quadrant, 32 columns each
+constexpr int TCA_DRAIN_COLS = 64 * 4 / TCA_DRAIN_WARPS;
+constexpr int TCA_MMA_WARP = TCA_DRAIN_WARP0 + TCA_DRAIN_WARPS;
+constexpr int TCA_THREADS = 32 * (TCA_MMA_WARP + 4);
+constexpr int TCA_DRAIN_REGS = TCA_DRAIN_WARPS == 4 ? 48 : 40;
 
 __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     const uint8_t* __restrict__ tinfo, const int32_t* __restrict__ n_tiles_p, int T, int d,
@@ -193,7 +205,10 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const AttnSmem L(T);
-  const uint8_t* info = smem + L.info;  // 4 tile-table slots (k_tile_info layout)
+  // 8 tile-table slots (k_tile_info layout): tile j + 8 is fetched at item
+  // (j + 7, 0), after the MMAs of item (j + 7) G - 2 and hence after the drain
+  // of item (j + 7) G - 4 >= j G read tile j's table
+  const uint8_t* info = smem + L.info;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint64_t* s_full = mbar + 0;
   uint64_t* s_free = mbar + 1;
@@ -201,11 +216,13 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   uint64_t* pv_done = mbar + 3;
   uint64_t* st_full = mbar + 4;     // [2]
   uint64_t* stage_free = mbar + 6;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 8);
+  uint64_t* o_empty = mbar + 8;     // [2]
+  uint64_t* info_ready = mbar + 10;  // [8]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 18);
   // exchange buffers alternate by head: a fast warp may publish head h+1
   // before a slow one of its quadrant has read head h
   __shared__ float2 red[2][4][128];  // (local max, local sum)
-  __shared__ float nrm[2][4][128];
+  __shared__ float2 dnrm[128];       // drain warps' partial row norms
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row = tid & 127, part = (tid >> 7) & 3;  // warp w owns TMEM lanes 32(w%4)..
   const int KBb = attn_kb_base(T);
@@ -226,7 +243,9 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&st_full[i], 3);  // the three producer warps
       tc::mbar_init(&stage_free[i], 1);
+      tc::mbar_init(&o_empty[i], TCA_DRAIN_WARPS);
     }
+    for (int i = 0; i < 8; ++i) tc::mbar_init(&info_ready[i], 3);
     tc::mbar_fence_init();
   }
   if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
@@ -235,16 +254,107 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t sb = tc::smem_u32(smem);
-  // TMEM columns: S_base | S_own | P (bf16 pairs) | O(group)
+  // TMEM columns: S_base | S_own | P (bf16 pairs) | O(even items) | O(odd items)
   const uint32_t TS_BASE = 0, TS_OWN = (uint32_t)TP, TS_P = (uint32_t)TP + 128,
                  TS_O = TS_P + (uint32_t)(TP + 128) / 2;
-  auto slot = [&](int j) { return info + (j & 3) * TINFO_BYTES; };
+  auto slot = [&](int j) { return info + (j & 7) * TINFO_BYTES; };
   auto kb_of = [&](int j) { return reinterpret_cast<const int32_t*>(slot(j) + 1548)[0]; };
 
-  if (warp >= TCA_SOFTMAX_WARPS) {
+  if (warp >= TCA_DRAIN_WARP0 && warp < TCA_MMA_WARP) {
+    // ================= drain warps: item O -> xh | xl and the row norms.
+    // Warp 16 + 4 h + q drains columns [h C, h C + C) of row quadrant q.
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(TCA_DRAIN_REGS) : "memory");
+    constexpr int C = TCA_DRAIN_COLS, NH = TCA_DRAIN_WARPS / 4;
+    const int q = warp & 3, hf = (warp - TCA_DRAIN_WARP0) >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t trq = tmem + ((uint32_t)(q * 32) << 16);
+    float xn2 = 0.f, rr2 = 0.f;
+    int dnloc = 0;
+    int64_t dloc0 = 0;
+    int j = 0, gi = 0;
+    for (int it = 0; it < nit; ++it) {
+      if (gi == 0) {
+        tc::mbar_wait(&info_ready[j & 7], (j >> 3) & 1);
+        const uint8_t* ti = slot(j);
+        dnloc = reinterpret_cast<const int32_t*>(ti + 1544)[0];
+        dloc0 = *reinterpret_cast<const int64_t*>(ti + 1536);
+        xn2 = 0.f;
+        rr2 = 0.f;
+      }
+      tc::mbar_wait(&stage_free[it & 1], (it >> 1) & 1);  // the item's O is complete
+      tc::fence_after();
+      const uint32_t ob = sb + L.out + (uint32_t)(row * ATT_OPITCH);
+#pragma unroll 1
+      for (int c16 = hf * C; c16 < hf * C + C; c16 += 16) {
+        float o[16];
+        tc::tmem_ld16(trq + TS_O + (uint32_t)((it & 1) * 64 + c16), o);
+        tc::tmem_wait_ld();
+        uint32_t ph[8], pl[8];
+#pragma unroll
+        for (int k = 0; k < 16; k += 2) {
+          ph[k / 2] = tc::pack_bf16(o[k], o[k + 1]);
+          const float h0 = __uint_as_float(ph[k / 2] << 16);
+          const float h1 = __uint_as_float(ph[k / 2] & 0xffff0000u);
+          pl[k / 2] = tc::pack_bf16(o[k] - h0, o[k + 1] - h1);
+          const float r0 = __uint_as_float(pl[k / 2] << 16);
+          const float r1 = __uint_as_float(pl[k / 2] & 0xffff0000u);  // |xl|^2 (tc_vq.cuh)
+          xn2 = fmaf(o[k], o[k], fmaf(o[k + 1], o[k + 1], xn2));
+          rr2 = fmaf(r0, r0, fmaf(r1, r1, rr2));
+        }
+        tc::st_shared_v4(ob + c16 * 2, ph[0], ph[1], ph[2], ph[3]);
+        tc::st_shared_v4(ob + c16 * 2 + 16, ph[4], ph[5], ph[6], ph[7]);
+        tc::st_shared_v4(ob + 128 * ATT_OPITCH + c16 * 2, pl[0], pl[1], pl[2], pl[3]);
+        tc::st_shared_v4(ob + 128 * ATT_OPITCH + c16 * 2 + 16, pl[4], pl[5], pl[6], pl[7]);
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&o_empty[it & 1]));  // O buffer free
+      // the warp's 32 rows x C columns, xh then xl: 64 segments of 2C bytes,
+      // C / 8 lanes per segment
+      constexpr int LPS = C / 8, SPI = 32 / LPS;
+#pragma unroll 4
+      for (int k = 0; k < 64 / SPI; ++k) {
+        const int seg = k * SPI + lane / LPS;  // 0..63
+        const int rr = q * 32 + (seg & 31);
+        const int cc = hf * C + (lane % LPS) * 8;
+        if (rr < dnloc) {
+          const uint32_t src = sb + L.out + (uint32_t)((seg >> 5) * 128 * ATT_OPITCH +
+                                                       rr * ATT_OPITCH + cc * 2);
+          uint32_t w0, w1, w2, w3;
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                       : "r"(src));
+          bf16* dst = ((seg >> 5) ? xl_out : xh_out) + (dloc0 + rr) * d + gi * 64 + cc;
+          *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
+        }
+      }
+      __syncwarp();
+      if (gi == G - 1) {
+        // row norms |x|^2 and |x - xh - xl|^2 over the tile's head groups
+        if constexpr (NH == 2) {
+          if (hf == 1) dnrm[row] = make_float2(xn2, rr2);
+          asm volatile("bar.sync %0, 64;" ::"r"(7 + q) : "memory");
+          if (hf == 0) {
+            const float2 o2 = dnrm[row];
+            xn2 += o2.x;
+            rr2 += o2.y;
+          }
+          asm volatile("bar.sync %0, 64;" ::"r"(7 + q) : "memory");
+        }
+        if (hf == 0 && row < dnloc) {
+          xn2_out[dloc0 + row] = xn2;
+          rr2_out[dloc0 + row] = rr2;
+        }
+      }
+      if (++gi == G) {
+        gi = 0;
+        ++j;
+      }
+    }
+  } else if (warp >= TCA_MMA_WARP) {
     // ================= MMA warp (one thread issues every tcgen05.mma)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
-    if (warp == TCA_SOFTMAX_WARPS && lane == 0 && nit > 0) {
+    if (warp == TCA_MMA_WARP && lane == 0 && nit > 0) {
       auto issue_scores = [&](int it, int hq, int kb_base) {
         const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
         const uint32_t qoff = (uint32_t)(hq * dh * 2);  // head offset inside the 128-B row
@@ -263,7 +373,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
         const uint32_t koff = (uint32_t)(hh * dh * 2);
         const uint32_t idO = tc::make_idesc_bf16(128, dh) | (1u << 16);
-        const uint32_t tO = tmem + TS_O + hh * dh, tA = tmem + TS_P;
+        const uint32_t tO = tmem + TS_O + (uint32_t)((it & 1) * 64 + hh * dh), tA = tmem + TS_P;
         const uint64_t db = tc::make_desc_sw128(st + L.vbase + koff);
         const uint64_t dw = tc::make_desc_sw128(st + L.vown + koff);
         // descriptor start field is address >> 4: 16 key rows = +128
@@ -304,6 +414,9 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           tc::fence_after();
           issue_scores(it2, hh2, kb_next);
         }
+        if (hh == 0 && it >= 2) {
+          tc::mbar_wait(&o_empty[it & 1], ((it - 2) >> 1) & 1);  // O buffer drained
+        }
         tc::mbar_wait(p_full, ph_p);  // every warp wrote P(g)
         ph_p ^= 1;
         tc::fence_after();
@@ -317,24 +430,30 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         kb_cur = kb_next;
       }
     }
-    if (warp > TCA_SOFTMAX_WARPS && nit > 0) {
+    if (warp > TCA_MMA_WARP && nit > 0) {
       // ================= producer warps: cp.async staging of every item into
       // its stage once the item two back has released it, tile tables one
       // tile ahead; three warps, 96 threads
-      const int ptid = tid - 32 * (TCA_SOFTMAX_WARPS + 1);
+      const int ptid = tid - 32 * (TCA_MMA_WARP + 1);
       auto pbar = [&]() { asm volatile("bar.sync 6, 96;" ::: "memory"); };
       auto fetch_info = [&](int j) {
         if (j < my_tiles)
           for (int c = ptid; c < TINFO_BYTES / 16; c += 96) {
             const uint8_t* src = tinfo + (int64_t)(blockIdx.x + j * gridDim.x) * TINFO_BYTES;
-            tc::cp_async16(sb + L.info + (uint32_t)((j & 3) * TINFO_BYTES) + c * 16, src + c * 16);
+            tc::cp_async16(sb + L.info + (uint32_t)((j & 7) * TINFO_BYTES) + c * 16, src + c * 16);
           }
+      };
+      auto info_arrive = [&](int t) {
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&info_ready[t & 7]));
       };
       fetch_info(0);
       fetch_info(1);
       tc::cp_async_commit();
       tc::cp_async_wait<0>();
       pbar();
+      info_arrive(0);
+      info_arrive(1);
       int j = 0, gi = 0;
       for (int it = 0; it < nit; ++it) {
         if (it >= 2) tc::mbar_wait(&stage_free[it & 1], ((it - 2) >> 1) & 1);
@@ -367,6 +486,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         pbar();  // every producer thread's copies (and the next table) landed
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&st_full[it & 1]));
+        if (gi == 0 && j >= 1) info_arrive(j + 1);
         if (++gi == G) {
           gi = 0;
           ++j;
@@ -375,7 +495,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     }
   } else {
     // ================= softmax / epilogue warps
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 96;" ::: "memory");
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const float sl2 = scale * 1.4426950408889634f;
     const uint32_t qbar = 1 + (warp & 3);  // named barrier of the row quadrant (128 threads)
@@ -388,7 +508,6 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     ATR_DECL
     // per-tile thread state
     bool live = false;
-    int64_t myloc = 0;
     int kb_base = 0;
     // per-tile chunk slots (slot i = chunk part + 4i of the warp's live chunks:
     // base chunks, then own chunks), packed once per tile:
@@ -396,8 +515,6 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     //   (entry j of the chunk is live iff 0 <= off + j < cnt); sflags bit i:
     //   slot live, bit 4 + i: every live row uses the whole chunk
     uint32_t sc_[4] = {0, 0, 0, 0}, oc_[4] = {0, 0, 0, 0}, sflags = 0;
-    float xn2 = 0.f, rr2 = 0.f;
-    int nloc = 0;
     int j = 0, gi = 0;  // item it = (j, gi)
     for (int it = 0; it < nit; ++it) {
       const int j1 = gi + 1 == G ? j + 1 : j, g1 = gi + 1 == G ? 0 : gi + 1;  // item it + 1
@@ -405,9 +522,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         // the table landed before any warp signalled this item's operands
         tc::mbar_wait(&st_full[it & 1], (it >> 1) & 1);
         const uint8_t* ti = slot(j);
-        nloc = reinterpret_cast<const int32_t*>(ti + 1544)[0];
-        live = row < nloc;
-        myloc = *reinterpret_cast<const int64_t*>(ti + 1536) + row;
+        live = row < reinterpret_cast<const int32_t*>(ti + 1544)[0];
         const int a = reinterpret_cast<const int16_t*>(ti + 1024)[row];
         const int own_lo = reinterpret_cast<const int16_t*>(ti + 1280)[row];
         const int own_cnt = live ? row - own_lo + 1 : 0;
@@ -434,13 +549,6 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           sflags |= (q < nq ? 1u : 0u) << i;
           sflags |= (full ? 1u : 0u) << (4 + i);
         }
-        xn2 = 0.f;
-        rr2 = 0.f;
-        // P columns no warp writes this tile must read as zero
-        const int pcols = (kb_base + 128) / 2;
-        const uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int c = part * 8; c < pcols; c += 32) tc::tmem_st8u(trow + TS_P + c, zero);
-        tc::tmem_wait_st();
       }
       ATR(12)
       for (int hh = 0; hh < hpg; ++hh) {
@@ -500,6 +608,21 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         ++hc;
         red[xb][part][row] = make_float2(mp, sp);
         ATR(2)
+        const bool pv_early = hh == 0 && gi == 0 && it > 0;
+        if (pv_early) {
+          // the previous item's last value MMA read P
+          tc::mbar_wait(pv_done, ph_o);
+          ph_o ^= 1;
+          tc::fence_after();
+        }
+        if (hh == 0 && gi == 0) {
+          // P columns no warp writes this tile must read as zero (before the
+          // quadrant barrier: another warpgroup may write these columns)
+          const int pcols = (kb_base + 128) / 2;
+          const uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          for (int c = part * 8; c < pcols; c += 32) tc::tmem_st8u(trow + TS_P + c, zero);
+          tc::tmem_wait_st();
+        }
         qsync();
         ATR(3)
         float2 rq[4];
@@ -513,7 +636,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         const float f = sp > 0.f ? __fdividef(ex2_approx((mp - m) * sl2), tot) : 0.f;
         ATR(4)
         // P is rewritten only after the previous head's value MMA consumed it
-        if (hh > 0) {
+        if ((hh > 0 || it > 0) && !pv_early) {
           tc::mbar_wait(pv_done, ph_o);
           ph_o ^= 1;
           tc::fence_after();
@@ -534,78 +657,15 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         arrive(p_full);  // O_h = P_base V_base + P_own V_own, issued by the MMA warp
         ATR(7)
       }
-      ATR(8)
-      tc::mbar_wait(pv_done, ph_o);  // the item's last value MMA
-      ph_o ^= 1;
-      tc::fence_after();
-      ATR(9)
-      // ---- drain O: warpgroup `part` takes columns [16 part, 16 part + 16) of
-      // its rows into the staging tile; the quadrant's four warps then store
-      // whole 128-B row segments
-      {
-        float o[16];
-        tc::tmem_ld16(trow + TS_O + part * 16, o);  // warp-collective: every lane loads
-        tc::tmem_wait_ld();
-        uint32_t ph[8], pl[8];
-#pragma unroll
-        for (int q = 0; q < 16; q += 2) {
-          ph[q / 2] = tc::pack_bf16(o[q], o[q + 1]);
-          const float h0 = __uint_as_float(ph[q / 2] << 16);
-          const float h1 = __uint_as_float(ph[q / 2] & 0xffff0000u);
-          pl[q / 2] = tc::pack_bf16(o[q] - h0, o[q + 1] - h1);
-          const float r0 = __uint_as_float(pl[q / 2] << 16);
-          const float r1 = __uint_as_float(pl[q / 2] & 0xffff0000u);  // |xl|^2 (tc_vq.cuh)
-          xn2 = fmaf(o[q], o[q], fmaf(o[q + 1], o[q + 1], xn2));
-          rr2 = fmaf(r0, r0, fmaf(r1, r1, rr2));
-        }
-        const uint32_t ob = sb + L.out + (uint32_t)(row * ATT_OPITCH + part * 32);
-        tc::st_shared_v4(ob, ph[0], ph[1], ph[2], ph[3]);
-        tc::st_shared_v4(ob + 16, ph[4], ph[5], ph[6], ph[7]);
-        tc::st_shared_v4(ob + 128 * ATT_OPITCH, pl[0], pl[1], pl[2], pl[3]);
-        tc::st_shared_v4(ob + 128 * ATT_OPITCH + 16, pl[4], pl[5], pl[6], pl[7]);
-        qsync();
-        // quadrant rows 32 q .. 32 q + 31, xh then xl: 64 segments of 128 B,
-        // 8 lanes per segment, 4 segments per warp instruction
-        const int q0 = (warp & 3) * 32;
-        const int64_t loc0 = myloc - row;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int seg = (part * 4 + k) * 4 + (lane >> 3);  // 0..63
-          const int rr = q0 + (seg & 31);
-          if (rr < nloc) {
-            const uint32_t src =
-                sb + L.out + (uint32_t)((seg >> 5) * 128 * ATT_OPITCH + rr * ATT_OPITCH +
-                                        (lane & 7) * 16);
-            uint32_t w0, w1, w2, w3;
-            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
-                         : "r"(src));
-            bf16* dst =
-                ((seg >> 5) ? xl_out : xh_out) + (loc0 + rr) * d + gi * 64 + (lane & 7) * 8;
-            *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
-          }
-        }
-      }
-      ATR(10)
-      if (gi == G - 1) {
-        // row norms |x|^2 and |x - xh - xl|^2, reduced over the quadrant's warps
-        nrm[0][part][row] = xn2;
-        nrm[1][part][row] = rr2;
-        qsync();
-        if (part == 0 && live) {
-          xn2_out[myloc] = ((nrm[0][0][row] + nrm[0][1][row]) + nrm[0][2][row]) + nrm[0][3][row];
-          rr2_out[myloc] = ((nrm[1][0][row] + nrm[1][1][row]) + nrm[1][2][row]) + nrm[1][3][row];
-        }
-      }
       ATR(11)
       j = j1;
       gi = g1;
     }
 #ifdef VQNQS_ATTN_TRACE
     if (blockIdx.x < 2 && lane == 0 && (warp == 0 || warp == 5 || warp == 10 || warp == 15))
-      printf("ATR b%d w%2d items %d: wS %llu ld %llu sm %llu bar %llu comb %llu wPV %llu P %llu arr %llu | end %llu wPVl %llu drain %llu nrm+pf %llu setup %llu\n",
+      printf("ATR b%d w%2d items %d: wS %llu ld %llu sm %llu bar %llu comb %llu wPV %llu P %llu arr %llu | end %llu setup %llu\n",
              blockIdx.x, warp, nit, atr[0], atr[1], atr[2], atr[3], atr[4], atr[5], atr[6], atr[7],
-             atr[8], atr[9], atr[10], atr[11], atr[12]);
+             atr[11], atr[12]);
 #endif
   }
   tc::fence_before();
