@@ -164,6 +164,34 @@ struct AttnSmem {
 #define ATR(k)
 #endif
 
+// exp2 of a pair on the FMA pipe, for moving part of the softmax exponentials
+// off the MUFU unit (16 lanes / clock / SM): 2^t = 2^n 2^f with n = rint(t),
+// f = t - n in [-1/2, 1/2], 2^f by a degree-5 minimax polynomial (relative
+// error 1.8e-7 in fp32 Horner, the accuracy of ex2.approx), 2^n added to the
+// exponent field. t is clamped to -127, where the result is exactly +0 (the
+// masked entries, t = -inf). VQNQS_ATTN_EMU_PAIRS of the 8 pairs per score
+// chunk take this path; measured on c4 / c5 0 is as fast as 2
+// and faster than 3 or 4: the softmax warps are latency-, not MUFU-bound.
+#ifndef VQNQS_ATTN_EMU_PAIRS
+#define VQNQS_ATTN_EMU_PAIRS 0
+#endif
+__device__ __forceinline__ float2 ex2_poly2(float2 t) {
+  constexpr float M = 12582912.0f;  // 1.5 * 2^23: t + M rounds t to an integer
+  t.x = fmaxf(t.x, -127.f);
+  t.y = fmaxf(t.y, -127.f);
+  const float2 j = tc::fadd2(t, make_float2(M, M));
+  const float2 n = tc::fadd2(j, make_float2(-M, -M));
+  const float2 f = tc::ffma2(n, make_float2(-1.f, -1.f), t);
+  float2 p = tc::ffma2(make_float2(1.3264698209241033e-3f, 1.3264698209241033e-3f), f,
+                       make_float2(9.671509265899658e-3f, 9.671509265899658e-3f));
+  p = tc::ffma2(p, f, make_float2(5.550733953714371e-2f, 5.550733953714371e-2f));
+  p = tc::ffma2(p, f, make_float2(2.4022242426872253e-1f, 2.4022242426872253e-1f));
+  p = tc::ffma2(p, f, make_float2(6.931470036506653e-1f, 6.931470036506653e-1f));
+  p = tc::ffma2(p, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -310,11 +338,15 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&o_empty[it & 1]));  // O buffer free
       // the warp's 32 rows x C columns, xh then xl: 64 segments of 2C bytes,
-      // C / 8 lanes per segment
+      // C / 8 lanes per segment. With C = 32 a shared-memory phase (8 lanes)
+      // reads two rows: rows 4 apart (16 banks apart at the 144-B pitch) so
+      // the two 64-B halves never share a bank.
       constexpr int LPS = C / 8, SPI = 32 / LPS;
+      const int sub = lane / LPS;
+      const int subr = SPI == 8 ? (((sub & 1) << 2) | (sub >> 1)) : sub;
 #pragma unroll 4
       for (int k = 0; k < 64 / SPI; ++k) {
-        const int seg = k * SPI + lane / LPS;  // 0..63
+        const int seg = k * SPI + subr;  // 0..63
         const int rr = q * 32 + (seg & 31);
         const int cc = hf * C + (lane % LPS) * 8;
         if (rr < dnloc) {
@@ -511,10 +543,10 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     int kb_base = 0;
     // per-tile chunk slots (slot i = chunk part + 4i of the warp's live chunks:
     // base chunks, then own chunks), packed once per tile:
-    //   sc_[i] = S column | P column << 9,  oc_[i] = (off + 512) | cnt << 10
-    //   (entry j of the chunk is live iff 0 <= off + j < cnt); sflags bit i:
-    //   slot live, bit 4 + i: every live row uses the whole chunk
-    uint32_t sc_[4] = {0, 0, 0, 0}, oc_[4] = {0, 0, 0, 0}, sflags = 0;
+    //   sc_[i] = S column | P column << 9; mk_[i >> 1] bits 16 (i & 1) + j:
+    //   entry j of the chunk is a key of the lane's row; sflags bit i: slot
+    //   live, bit 4 + i: every live row uses the whole chunk
+    uint32_t sc_[4] = {0, 0, 0, 0}, mk_[2] = {0, 0}, sflags = 0;
     int j = 0, gi = 0;  // item it = (j, gi)
     for (int it = 0; it < nit; ++it) {
       const int j1 = gi + 1 == G ? j + 1 : j, g1 = gi + 1 == G ? 0 : gi + 1;  // item it + 1
@@ -535,6 +567,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         const int nb = wb_end >> 4;
         const int nq = nb + max(0, (wo_end - wo_beg) >> 4);
         sflags = 0;
+        mk_[0] = mk_[1] = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int q = part + 4 * i;
@@ -544,7 +577,9 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           const int cnt = isb ? a : own_cnt;
           sc_[i] = (uint32_t)((isb ? TS_BASE : TS_OWN) + c0) |
                    ((uint32_t)((isb ? c0 : kb_base + c0) >> 1) << 9);
-          oc_[i] = (uint32_t)(off + 512) | ((uint32_t)cnt << 10);
+          const int lo = max(0, -off), hi = min(16, cnt - off);
+          const uint32_t m16 = (live && hi > lo) ? ((1u << hi) - 1u) & ~((1u << lo) - 1u) : 0u;
+          mk_[i >> 1] |= m16 << (16 * (i & 1));
           const bool full = __all_sync(0xffffffffu, !live || (off >= 0 && off + 16 <= cnt));
           sflags |= (q < nq ? 1u : 0u) << i;
           sflags |= (full ? 1u : 0u) << (4 + i);
@@ -561,14 +596,11 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         // part + 4i. ONE TMEM pass loads them into registers.
         float v[4][16];
         bool sl[4], full[4];
-        int off[4], cnt[4];
         uint32_t pcol[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           sl[i] = (sflags >> i) & 1u;
           full[i] = (sflags >> (4 + i)) & 1u;
-          off[i] = (int)(oc_[i] & 1023u) - 512;
-          cnt[i] = (int)(oc_[i] >> 10);
           pcol[i] = sc_[i] >> 9;
           if (sl[i]) tc::tmem_ld16(trow + (sc_[i] & 511u), v[i]);
         }
@@ -585,25 +617,35 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
 #pragma unroll
             for (int q = 0; q < 16; ++q) mp = fmaxf(mp, v[i][q]);
           } else {
+            const uint32_t m16 = mk_[i >> 1] >> (16 * (i & 1));
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-              const bool ok = (unsigned)(off[i] + q) < (unsigned)cnt[i];
-              v[i][q] = ok ? v[i][q] : -INFINITY;
+              v[i][q] = (m16 >> q) & 1u ? v[i][q] : -INFINITY;
               mp = fmaxf(mp, v[i][q]);
             }
           }
         }
         const float mref = mp == -INFINITY ? 0.f : mp * sl2;
-        float sp = 0.f;
+        float2 sp2 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           if (!sl[i]) continue;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            v[i][q] = ex2_approx(fmaf(v[i][q], sl2, -mref));
-            sp += v[i][q];
+          for (int q = 0; q < 16; q += 2) {
+            const float2 t = tc::ffma2(make_float2(v[i][q], v[i][q + 1]), make_float2(sl2, sl2),
+                                       make_float2(-mref, -mref));
+            if (q / 2 < 8 - VQNQS_ATTN_EMU_PAIRS) {
+              v[i][q] = ex2_approx(t.x);
+              v[i][q + 1] = ex2_approx(t.y);
+            } else {
+              const float2 e = ex2_poly2(t);
+              v[i][q] = e.x;
+              v[i][q + 1] = e.y;
+            }
+            sp2 = tc::fadd2(sp2, make_float2(v[i][q], v[i][q + 1]));
           }
         }
+        const float sp = sp2.x + sp2.y;
         const int xb = hc & 1;
         ++hc;
         red[xb][part][row] = make_float2(mp, sp);
@@ -648,7 +690,10 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           if (!sl[i]) continue;
           uint32_t pk[8];
 #pragma unroll
-          for (int q = 0; q < 16; q += 2) pk[q / 2] = tc::pack_bf16(v[i][q] * f, v[i][q + 1] * f);
+          for (int q = 0; q < 16; q += 2) {
+            const float2 p2 = tc::fmul2(make_float2(v[i][q], v[i][q + 1]), make_float2(f, f));
+            pk[q / 2] = tc::pack_bf16(p2.x, p2.y);
+          }
           tc::tmem_st8u(trow + TS_P + pcol[i], pk);
         }
         tc::tmem_wait_st();
