@@ -348,6 +348,7 @@ __global__ void kg_vq_fwd(int64_t R, int d, int Q, const float* __restrict__ x,
       jb = oj;
     }
   }
+  if (jb == 0x7fffffff) jb = 0;  // no finite distance: the reference's argmin keeps index 0
   if (lane == 0) pick[r] = jb;
   const float* w = cb + (int64_t)__shfl_sync(0xffffffffu, jb, 0) * d;
   for (int c = lane; c < d; c += 32) xq[r * d + c] = w[c];

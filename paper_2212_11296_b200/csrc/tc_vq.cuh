@@ -355,7 +355,9 @@ __global__ void __launch_bounds__(256) k_vq_rescore(
         jb = oj;
       }
     }
-    if (lane == 0) code[row] = jb;
+    // no finite distance (x or the codebook not finite): the reference's
+    // argmin keeps its initial index 0 (proj/src/model.cpp:283-319)
+    if (lane == 0) code[row] = jb == 0x7fffffff ? 0 : jb;
   }
   if (n_rescored && lane == 0 && done) atomicAdd(n_rescored, done);
 }
