@@ -25,15 +25,16 @@
 // warpgroups exchange (local max, local sum) once, write the normalised bf16
 // probabilities straight back to TMEM, and the value product takes P as its
 // TMEM A operand (no shared-memory round trip). The next head's score MMA is
-// issued as soon as every warp holds its scores; the next item's first score
-// MMA runs while this item's O drains.
-// TMEM: S_base | S_own | P (bf16 pairs) | O(group) = 1.5 (T_pad + 128) + 64 <= 512.
+// issued as soon as every warp holds its scores; dedicated drain warps empty
+// an item's O while the softmax warps work on the next item.
+// TMEM: S_base | S_own | P (bf16 pairs) | O(even item) | O(odd item)
+//       = 1.5 (T_pad + 128) + 128 <= 512.
 //
 // Outputs per active location: the attention row x as its two-term bf16
 // split xh = bf16(x), xl = bf16(x - xh) (the VQ distance GEMM operands; x is
 // represented to 2^-18 relative), |x|^2 and |x - xh - xl|^2 (the certified
-// argmin error bound, tc_vq.cuh). 512 threads: warp w owns TMEM lanes
-// 32(w%4).. (its query rows).
+// argmin error bound, tc_vq.cuh). Warp w reads TMEM lanes 32(w%4).. (its
+// query rows); the warp roles are listed at TCA_THREADS.
 #pragma once
 
 #include "common.cuh"

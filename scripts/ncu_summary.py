@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (developer tool; needs `ncu` on PATH).
 
-    python scripts/ncu_summary.py full  REP.ncu-rep OUT.txt     # --set full capture
+    python scripts/ncu_summary.py full  REP.ncu-rep[#i] OUT.txt # --set full capture (i-th kernel)
     python scripts/ncu_summary.py launches LAUNCHES.csv OUT.txt # gpu__time_duration list
     python scripts/ncu_summary.py traffic OUT.json NAME=REP.ncu-rep ... --note "..."
 """
@@ -23,10 +23,15 @@ KEYS = [
 
 
 def raw(rep):
+    """(header, units, values) of kernel i of REP#i (default 0)."""
+    idx = 0
+    if "#" in rep:
+        rep, i = rep.rsplit("#", 1)
+        idx = int(i)
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     r = list(csv.reader(out.splitlines()))
-    return r[0], r[1], r[2]
+    return r[0], r[1], r[2 + idx]
 
 
 def to_bytes(v, unit):
