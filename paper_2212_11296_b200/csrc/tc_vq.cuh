@@ -44,7 +44,7 @@ constexpr int TCV_QCAND = TCV_EPI_PARTS * TCV_CAND;  // queued survivors per row
 
 inline size_t tcv_smem_bytes(int Q) {
   return 1024 + size_t(TCV_STAGES) * TCV_STAGE_BYTES + 256 + size_t(Q) * 4 +
-         size_t(TCV_EPI_PARTS) * 128 * 12 + 64;
+         2 * size_t(TCV_EPI_PARTS) * 128 * 12 + 64;
 }
 
 __device__ __forceinline__ double vq_exact_d2(const bf16* __restrict__ xh,
@@ -117,9 +117,11 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float* wn2 = reinterpret_cast<float*>(tail + 256);
-  float* red_min = wn2 + Q;                                              // [parts][128]
-  int* red_cnt = reinterpret_cast<int*>(red_min + TCV_EPI_PARTS * 128);  // [parts][128]
-  int* red_jf = red_cnt + TCV_EPI_PARTS * 128;                           // [parts][128]
+  // per-row merge scratch, double-buffered by tile parity (no barrier needed
+  // before the next tile reuses it)
+  float* red_min0 = wn2 + Q;                                               // [2][parts][128]
+  int* red_cnt0 = reinterpret_cast<int*>(red_min0 + 2 * TCV_EPI_PARTS * 128);  // [2][parts][128]
+  int* red_jf0 = red_cnt0 + 2 * TCV_EPI_PARTS * 128;                           // [2][parts][128]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t M = *Mp;
   const int KB = d / 64;
@@ -221,11 +223,29 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
     constexpr int PW = TCV_NCH / TCV_EPI_PARTS;
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     uint32_t acc = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    // the row norms are loaded one tile ahead (their latency would otherwise
+    // sit in front of every tile's first accumulator)
+    float xn2_nx = 0.f, xl2_nx = 0.f;
+    if (blockIdx.x < n_tiles && (int64_t)blockIdx.x * 128 + row < M) {
+      xn2_nx = xn2g[(int64_t)blockIdx.x * 128 + row];
+      xl2_nx = xl2g[(int64_t)blockIdx.x * 128 + row];
+    }
+    int tpar = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, tpar ^= 1) {
       const int64_t my = t * 128 + row;
       const bool live = my < M;
-      const float xn = live ? sqrtf(xn2g[my]) : 0.f;
-      const float xln = live ? sqrtf(xl2g[my]) : 0.f;
+      const float xn = live ? sqrtf(xn2_nx) : 0.f;
+      const float xln = live ? sqrtf(xl2_nx) : 0.f;
+      {
+        const int64_t myn = (t + gridDim.x) * 128 + row;
+        if (t + gridDim.x < n_tiles && myn < M) {
+          xn2_nx = xn2g[myn];
+          xl2_nx = xl2g[myn];
+        }
+      }
+      float* red_min = red_min0 + tpar * TCV_EPI_PARTS * 128;
+      int* red_cnt = red_cnt0 + tpar * TCV_EPI_PARTS * 128;
+      int* red_jf = red_jf0 + tpar * TCV_EPI_PARTS * 128;
       // |r| <= 2^-8 / (1 - 2^-8) |xl|: the residual of the two-term split
       const float E = 2.f * (0.00393f * xln * wmax + float(d) * 1.2e-7f * xn * wmax) +
                       4e-7f * (wmax * wmax + 2.f * xn * wmax);
@@ -252,9 +272,20 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
           if (vmin <= run_min + w2) {  // rare once the running minimum settles
             run_min = fminf(run_min, vmin);
             const float thr = run_min + w2;
+            // the lane's survivors as a bit mask, then one insertion per set
+            // bit (j ascending): a lane pays for its own candidates only,
+            // instead of the warp stepping through 32 divergent insertions
+            uint32_t m = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (v[j] <= thr) cand_add(C, v[j], jbase + j, thr);
+            for (int j = 0; j < 32; ++j) m |= (v[j] <= thr ? 1u : 0u) << j;
+            while (m) {
+              const int j = __ffs(m) - 1;
+              m &= m - 1;
+              float dv = v[0];
+#pragma unroll
+              for (int q = 1; q < 32; ++q) dv = q == j ? v[q] : dv;
+              cand_add(C, dv, jbase + j, thr);
+            }
           }
         }
         tc::fence_before();
@@ -303,7 +334,9 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
           }
         }
       }
-      epi_bar();
+      // no barrier here: the next tile merges through the other scratch
+      // buffer, and its first barrier orders this tile's reads before the
+      // tile after next overwrites this buffer
     }
   }
   __syncthreads();
