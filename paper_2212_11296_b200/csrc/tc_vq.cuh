@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
     const int row = (warp & 3) * 32 + lane;
     const int part = (warp - 2) >> 2;  // columns [PW part, PW part + PW) of a chunk
     constexpr int PW = TCV_NCH / TCV_EPI_PARTS;
+    static_assert(PW == 64, "the epilogue loads a part as two 32-column groups");
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     uint32_t acc = 0;
     // the row norms are loaded one tile ahead (their latency would otherwise
@@ -258,11 +259,15 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
         const uint32_t b = acc & 1;
         tc::mbar_wait(&acc_full[b], (acc >> 1) & 1);
         tc::fence_after();
-        for (int c0 = part * PW; c0 < part * PW + PW; c0 += 32) {
-          float v[32];
-          tc::tmem_ld32(trow + b * TCV_NCH + c0, v);
-          tc::tmem_wait_ld();
-          const int jbase = c * TCV_NCH + c0;
+        // both 32-column groups of the part are loaded before one wait
+        float vv[2][32];
+        tc::tmem_ld32(trow + b * TCV_NCH + part * PW, vv[0]);
+        tc::tmem_ld32(trow + b * TCV_NCH + part * PW + 32, vv[1]);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          float* v = vv[g];
+          const int jbase = c * TCV_NCH + part * PW + 32 * g;
           float vmin = INFINITY;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -278,13 +283,14 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
             uint32_t m = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) m |= (v[j] <= thr ? 1u : 0u) << j;
+            // each survivor is recorded with the group minimum, a lower bound
+            // of its distance: later pruning (d <= threshold) then keeps a
+            // superset of the rows' true survivors, which only the exact
+            // re-scoring can shrink (never drops the argmin)
             while (m) {
               const int j = __ffs(m) - 1;
               m &= m - 1;
-              float dv = v[0];
-#pragma unroll
-              for (int q = 1; q < 32; ++q) dv = q == j ? v[q] : dv;
-              cand_add(C, dv, jbase + j, thr);
+              cand_add(C, vmin, jbase + j, thr);
             }
           }
         }
