@@ -264,19 +264,26 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
         tc::tmem_ld32(trow + b * TCV_NCH + part * PW, vv[0]);
         tc::tmem_ld32(trow + b * TCV_NCH + part * PW + 32, vv[1]);
         tc::tmem_wait_ld();
+        float gm[2];
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
-          float* v = vv[g];
           const int jbase = c * TCV_NCH + part * PW + 32 * g;
-          float vmin = INFINITY;
+          gm[g] = INFINITY;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            v[j] = fmaf(-2.f, v[j], wn2[jbase + j]);
-            vmin = fminf(vmin, v[j]);
+            vv[g][j] = fmaf(-2.f, vv[g][j], wn2[jbase + j]);
+            gm[g] = fminf(gm[g], vv[g][j]);
           }
-          if (vmin <= run_min + w2) {  // rare once the running minimum settles
-            run_min = fminf(run_min, vmin);
-            const float thr = run_min + w2;
+        }
+        // the threshold uses both groups' minima, so a group is scanned for
+        // survivors only when it holds (or nearly holds) the running minimum
+        run_min = fminf(run_min, fminf(gm[0], gm[1]));
+        const float thr = run_min + w2;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          if (gm[g] <= thr) {  // rare once the running minimum settles
+            const float* v = vv[g];
+            const int jbase = c * TCV_NCH + part * PW + 32 * g;
             // the lane's survivors as a bit mask, then one insertion per set
             // bit (j ascending): a lane pays for its own candidates only,
             // instead of the warp stepping through 32 divergent insertions
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
             while (m) {
               const int j = __ffs(m) - 1;
               m &= m - 1;
-              cand_add(C, vmin, jbase + j, thr);
+              cand_add(C, gm[g], jbase + j, thr);
             }
           }
         }
