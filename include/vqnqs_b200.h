@@ -185,7 +185,7 @@ int64_t vqnqs_gpu_last_launch_count(vqnqs_handle* h);
  * [0] attention+VQ ms  [1] their algorithmic flops  [2] launches timed
  * [3] active locations  [4] sum U_b  [5] sum U_{b+1}  [6] VQ ms
  * [7] attention ms  [8] VQ rows re-scored  [9] attention flops
- * [10] VQ distance flops  [11] reserved. */
+ * [10] VQ distance flops  [11] attention tiles (<= 128 active locations each). */
 int vqnqs_gpu_last_profile(vqnqs_handle* h, double* out, int cap);
 
 int vqnqs_gpu_destroy(vqnqs_handle* h);

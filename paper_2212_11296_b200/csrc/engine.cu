@@ -618,6 +618,9 @@ class EngineImpl {
     CK(cudaMemcpyAsync(haw.data(), attw_.p, S * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hK.data(), K_.p, S * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hU.data(), Ucnt_.p, hU.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    int32_t h_ntiles = 0;
+    if (use_tc_attn)
+      CK(cudaMemcpyAsync(&h_ntiles, ntiles_.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     if (taps) {
       tap_act_off->resize(S);
       tap_t1->resize(R);
@@ -645,6 +648,7 @@ class EngineImpl {
     prof[9] += double(L) * 4.0 * d * aw;            // attention (QK^T + PV, live keys)
     prof[10] += double(L) * 2.0 * double(d) * Q * double(M);  // VQ distance GEMM
     prof[3] += double(M) * L;
+    prof[11] += double(h_ntiles) * L;  // attention tiles (<= 128 locations each)
     for (int s2 = 0; s2 < S; ++s2)
       for (int b = 0; b < L; ++b) {
         prof[4] += hU[size_t(b) * S + s2];

@@ -2,7 +2,7 @@
 of one batch per workload plus the engine's stage profile.
 
     python scripts/quickbench.py c3_10x10:1024 c4_16x16:1024 c5_12x12:1024
-prints: workload evals/s ms/step attention_ms vq_ms rescored
+prints: workload evals/s ms/step attention_ms vq_ms rescored tile_fill (locations per tile)
 """
 import sys
 import time
@@ -32,8 +32,9 @@ def run(name: str, batch: int, steps: int = 3) -> None:
     ms = (time.perf_counter() - t0) * 1e3 / steps
     prof = eng.last_profile()
     evals = led.other // w.model.seq_len  # connected configurations
-    print(f"{name} {evals / ms * 1e3:.0f} {ms:.1f} {prof[7]:.1f} {prof[6]:.1f} {prof[8]:.0f}",
-          flush=True)
+    fill = prof[3] / prof[11] if len(prof) > 11 and prof[11] else 0.0
+    print(f"{name} {evals / ms * 1e3:.0f} {ms:.1f} {prof[7]:.1f} {prof[6]:.1f} {prof[8]:.0f} "
+          f"tile_fill={fill:.1f}", flush=True)
 
 
 if __name__ == "__main__":
