@@ -10,11 +10,14 @@
 //   warp 1   MMA issuer: acc_j = xh . W_j + xl . W_j, 256 codes per
 //            accumulator, two TMEM accumulators (512 columns) so the
 //            epilogue of one code chunk overlaps the MMAs of the next;
-//   warps 2-9 epilogue (two warpgroups, 128 columns each): D~_j =
-//            |W_j|^2 - 2 acc_j is within E = 2(|r| + d 2^-23 |x|) max|W| +
-//            slack of the exact D_j(x) - |x|^2, so every code with
-//            D~_j <= running min + 2E is kept (<= 8 per warpgroup); a single
-//            survivor is the answer, otherwise the row and its survivors go to
+//   warps 2-17 epilogue (four per TMEM lane quadrant, 64 columns of each
+//            accumulator each): D~_j = |W_j|^2 - 2 acc_j is within
+//            E = 2(|r| + d 2^-23 |x|) max|W| + slack of the exact
+//            D_j(x) - |x|^2, so every code with D~_j <= running min + 2E is
+//            kept (<= 8 per part; a part scans a 32-column group only when its
+//            minimum comes within 2E of the running minimum, by a bit mask of
+//            the survivors); a single survivor is the answer, otherwise the
+//            row and its survivors go to
 //            a queue and k_vq_rescore re-scores them as
 //            sum_c ((xh + xl)_c - W_jc)^2 in double, c ascending — the
 //            reference's own arithmetic (proj/src/model.cpp:298-303) — and the
