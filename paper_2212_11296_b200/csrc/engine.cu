@@ -15,6 +15,7 @@
 // chunk's active-location/table totals (to size the arena) and the final
 // U-count readback for the ledger.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -376,7 +377,9 @@ class EngineImpl {
     // in the no-reuse regime every row is active in full
     const double locs = double(T) + double(nb) * (dense ? 0.5 : 0.25) * double(T);
     const double bytes_per_loc = double(d) * 40.0 + 64.0;
-    const double budget = 40e9;
+    // working-set budget per micro-batch (VQNQS_CHUNK_GB overrides, for tuning)
+    double budget = 80e9;
+    if (const char* e = std::getenv("VQNQS_CHUNK_GB")) budget = std::max(1.0, std::atof(e)) * 1e9;
     S_max = int(std::clamp(budget / (locs * bytes_per_loc), 16.0, 4096.0));
   }
   void set_reuse(bool reuse) {
