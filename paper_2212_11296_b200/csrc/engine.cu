@@ -167,6 +167,8 @@ class EngineImpl {
   DBuf<uint8_t> tinfo_;
   VqScratch vqs_;  // deferred VQ re-scoring queue
   DBuf<int32_t> ntiles_;
+  DBuf<int32_t> tcnt_;  // attention tiles per sample
+  DBuf<int64_t> toff_;  // their exclusive scan, [S] = total
   DBuf<double> out_stage_;
   DBuf<int32_t> taps_codes_;
   size_t tab_cap_n = 0;
@@ -508,10 +510,16 @@ class EngineImpl {
         // tiles of whole rows (once per chunk; rows do not change across layers)
         if (b == 0) {
           tiles_.ensure(R);
-          CK(cudaMemsetAsync(ntiles_.p, 0, sizeof(int32_t), st));
-          k_build_tiles<<<(S + 127) / 128, 128, 0, st>>>(S, R1, T, K_.p, row_t1_.p, row_perm_.p,
-                                                         act_off_.p, tiles_.p, ntiles_.p);
-          ++launches;
+          tcnt_.ensure(S);
+          toff_.ensure(S + 1);
+          k_build_tiles<<<(S + 127) / 128, 128, 0, st>>>(0, S, R1, T, K_.p, row_t1_.p,
+                                                         row_perm_.p, act_off_.p, tcnt_.p, nullptr,
+                                                         nullptr, tiles_.p, ntiles_.p);
+          k_scan<<<1, 1024, 0, st>>>(S, tcnt_.p, toff_.p, toff_.p + S, 0);
+          k_build_tiles<<<(S + 127) / 128, 128, 0, st>>>(1, S, R1, T, K_.p, row_t1_.p,
+                                                         row_perm_.p, act_off_.p, tcnt_.p,
+                                                         toff_.p, toff_.p + S, tiles_.p, ntiles_.p);
+          launches += 3;
         }
         // per-layer tile tables (qkv rows follow this layer's dedup); at most
         // 2 M / 128 + 3 S tiles (two consecutive tiles of a sample hold > 128)

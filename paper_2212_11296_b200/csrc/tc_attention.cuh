@@ -50,33 +50,42 @@ struct AttnTile {
 };
 
 // Greedy packing of whole rows (consecutive in active-location order) into
-// tiles of <= 128 locations, one thread per sample.
-__global__ void k_build_tiles(int S, int R1, int T, const int32_t* __restrict__ K,
+// tiles of <= 128 locations, one thread per sample, in two passes: pass 0
+// counts each sample's tiles (tcnt), pass 1 writes them at the sample's
+// exclusive-scan offset (toff, k_scan) so a sample's tiles are contiguous in
+// the tile list. The persistent attention kernel deals tiles round-robin over
+// the CTAs, so the CTAs then work on the same few samples at a time and the
+// samples' shared base-row K/V stay in L2.
+__global__ void k_build_tiles(int pass, int S, int R1, int T, const int32_t* __restrict__ K,
                               const int32_t* __restrict__ row_t1,
                               const int32_t* __restrict__ row_perm,
-                              const int64_t* __restrict__ act_off, AttnTile* __restrict__ tiles,
-                              int32_t* __restrict__ n_tiles) {
+                              const int64_t* __restrict__ act_off, int32_t* __restrict__ tcnt,
+                              const int64_t* __restrict__ toff, const int64_t* __restrict__ ttot,
+                              AttnTile* __restrict__ tiles, int32_t* __restrict__ n_tiles) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pass == 1 && s == 0) *n_tiles = (int32_t)*ttot;
   if (s >= S) return;
   const int Ks = K[s];
-  int cur = 0;
+  int cur = 0, nt = 0;
   int64_t start = act_off[s];
+  const int64_t base = pass == 1 ? toff[s] : 0;
   for (int i = 0; i < Ks; ++i) {  // rows in active-layout order (k_connected)
     const int k = row_perm[(int64_t)s * R1 + i];
     const int n = k == 0 ? T : T - (row_t1[(int64_t)s * R1 + k] + 1);
     if (n <= 0) continue;
     if (cur + n > 128) {
-      const int t = atomicAdd(n_tiles, 1);
-      tiles[t] = AttnTile{s, cur, start};
+      if (pass == 1) tiles[base + nt] = AttnTile{s, cur, start};
+      ++nt;
       start += cur;
       cur = 0;
     }
     cur += n;
   }
   if (cur > 0) {
-    const int t = atomicAdd(n_tiles, 1);
-    tiles[t] = AttnTile{s, cur, start};
+    if (pass == 1) tiles[base + nt] = AttnTile{s, cur, start};
+    ++nt;
   }
+  if (pass == 0) tcnt[s] = nt;
 }
 
 __host__ __device__ inline int attn_tpad(int T) { return ((T + 15) / 16) * 16; }
