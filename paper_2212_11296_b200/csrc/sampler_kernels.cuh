@@ -32,6 +32,9 @@ __global__ void k_dec_embed(int B, int d, int T, int V, int t, const int32_t* __
 // Products are formed from the stored operands (bf16 in the bf16 configs)
 // with fp32 accumulation; in bf16 mode P is rounded to bf16 before the value
 // product, where the reference's emulated product boundary rounds.
+// Scores: a group of dh/4 lanes takes one key (4 dims per lane, one
+// contiguous dh-element row read per group) and reduces with shuffles, so a
+// warp scores 128/dh keys per step with coalesced loads.
 template <typename TA>
 __global__ void k_dec_attention(int B, int d, int nh, int T, int t, float scale,
                                 const TA* __restrict__ qkv, TA* __restrict__ Kc,
@@ -55,15 +58,40 @@ __global__ void k_dec_attention(int B, int d, int nh, int T, int t, float scale,
   }
   __syncwarp();
   float m = -INFINITY;
-  for (int j = lane; j <= t; j += 32) {
-    const TA* kj = kc + (int64_t)j * d;
-    float s = 0.f;
-    for (int e = 0; e < dh; ++e) s = fmaf(q[e], to_f<TA>(kj[e]), s);
-    s *= scale;
-    P[j] = s;
-    m = fmaxf(m, s);
+  const bool grouped = dh % 4 == 0 && dh <= 128 && ((dh / 4) & (dh / 4 - 1)) == 0;
+  if (grouped) {
+    const int lpk = dh / 4, kpi = 32 / lpk;  // lanes per key, keys per step
+    const int sub = lane % lpk, kq = lane / lpk;
+    float q4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) q4[e] = q[sub * 4 + e];
+    for (int j0 = 0; j0 <= t; j0 += kpi) {
+      const int j = j0 + kq;
+      float s = 0.f;
+      if (kq < kpi && j <= t) {
+        const TA* kj = kc + (int64_t)j * d + sub * 4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s = fmaf(q4[e], to_f<TA>(kj[e]), s);
+      }
+      for (int o = lpk >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (kq < kpi && j <= t && sub == 0) {
+        s *= scale;
+        P[j] = s;
+        m = fmaxf(m, s);
+      }
+    }
+  } else {
+    for (int j = lane; j <= t; j += 32) {
+      const TA* kj = kc + (int64_t)j * d;
+      float s = 0.f;
+      for (int e = 0; e < dh; ++e) s = fmaf(q[e], to_f<TA>(kj[e]), s);
+      s *= scale;
+      P[j] = s;
+      m = fmaxf(m, s);
+    }
   }
   m = warp_max(m);
+  __syncwarp();
   float sum = 0.f;
   for (int j = lane; j <= t; j += 32) {
     const float e = expf(P[j] - m);
@@ -74,10 +102,31 @@ __global__ void k_dec_attention(int B, int d, int nh, int T, int t, float scale,
   const float inv = 1.f / sum;
   for (int j = lane; j <= t; j += 32) P[j] = to_f<TA>(from_f<TA>(P[j] * inv));
   __syncwarp();
-  for (int e = lane; e < dh; e += 32) {
-    float acc = 0.f;
-    for (int j = 0; j <= t; ++j) acc = fmaf(P[j], to_f<TA>(vc[(int64_t)j * d + e]), acc);
-    o[(int64_t)b * d + h * dh + e] = acc;
+  if (grouped) {
+    // values: the same lane groups, 4 dims per lane, keys strided by group,
+    // then a shuffle reduction across the groups
+    const int lpk = dh / 4, kpi = 32 / lpk;
+    const int sub = lane % lpk, kq = lane / lpk;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = kq; j <= t; j += kpi) {
+      const TA* vj = vc + (int64_t)j * d + sub * 4;
+      const float pj = P[j];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] = fmaf(pj, to_f<TA>(vj[e]), acc[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      for (int off = lpk; off < 32; off <<= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], off);
+    if (kq == 0) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[(int64_t)b * d + h * dh + sub * 4 + e] = acc[e];
+    }
+  } else {
+    for (int e = lane; e < dh; e += 32) {
+      float acc = 0.f;
+      for (int j = 0; j <= t; ++j) acc = fmaf(P[j], to_f<TA>(vc[(int64_t)j * d + e]), acc);
+      o[(int64_t)b * d + h * dh + e] = acc;
+    }
   }
 }
 
