@@ -317,6 +317,89 @@ __global__ void kg_attn_bwd(int T, int d, int nh, float sc, const float* __restr
 // VQ forward (autodiff.cpp:536-580, gumbel off): distances in double, c
 // ascending; argmin with ties to the lowest index. Warp per row. Keeps
 // |x - W_j| for the surrogate backward.
+// Block-tiled VQ forward: 32 rows per block (8 warps x 4 rows), codes in
+// chunks of 32 staged in shared memory (lane = code, row stride d + 1: no bank
+// conflicts), the rows' x in shared memory; per (row, code) the same
+// sequential double sum over c as kg_vq_fwd, so results are identical.
+constexpr int KGVQ_ROWS = 32;
+inline size_t kg_vq_tiled_smem(int d) { return size_t(KGVQ_ROWS) * (2 * d + 1) * sizeof(float); }
+__global__ void __launch_bounds__(256) kg_vq_fwd_tiled(int64_t R, int d, int Q,
+                                                       const float* __restrict__ x,
+                                                       const float* __restrict__ cb,
+                                                       float* __restrict__ dist,
+                                                       int* __restrict__ pick,
+                                                       float* __restrict__ xq) {
+  extern __shared__ float sm[];
+  float* Xs = sm;                         // [32 rows][d]
+  float* Ws = sm + KGVQ_ROWS * d;         // [32 codes][d + 1]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * KGVQ_ROWS;
+  for (int i = threadIdx.x; i < KGVQ_ROWS * d; i += blockDim.x) {
+    const int64_t r = r0 + i / d;
+    Xs[i] = r < R ? x[r0 * d + i] : 0.f;
+  }
+  double best[4];
+  int jb[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    best[k] = 1e300;
+    jb[k] = 0x7fffffff;
+  }
+  for (int j0 = 0; j0 < Q; j0 += 32) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * d; i += blockDim.x) {
+      const int jj = i / d, c = i % d;
+      Ws[jj * (d + 1) + c] = j0 + jj < Q ? cb[(int64_t)(j0 + jj) * d + c] : 0.f;
+    }
+    __syncthreads();
+    const int j = j0 + lane;
+    double s2[4] = {0.0, 0.0, 0.0, 0.0};
+    const float* wr = Ws + lane * (d + 1);
+    for (int c = 0; c < d; ++c) {
+      const double wc = double(wr[c]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double df = double(Xs[(w + 8 * k) * d + c]) - wc;
+        s2[k] += df * df;
+      }
+    }
+    if (j < Q) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t r = r0 + w + 8 * k;
+        if (r < R) {
+          dist[r * Q + j] = float(sqrt(s2[k]));
+          if (s2[k] < best[k]) {  // j ascending per lane: strict < keeps the lowest index
+            best[k] = s2[k];
+            jb[k] = j;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double bk = best[k];
+    int jk = jb[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, jk, o);
+      if (ob < bk || (ob == bk && oj < jk)) {
+        bk = ob;
+        jk = oj;
+      }
+    }
+    if (jk == 0x7fffffff) jk = 0;  // no finite distance: the reference's argmin keeps index 0
+    const int64_t r = r0 + w + 8 * k;
+    if (r < R) {
+      if (lane == 0) pick[r] = jk;
+      const float* wq = cb + (int64_t)jk * d;
+      for (int c = lane; c < d; c += 32) xq[r * d + c] = wq[c];
+    }
+  }
+}
+
 __global__ void kg_vq_fwd(int64_t R, int d, int Q, const float* __restrict__ x,
                           const float* __restrict__ cb, float* __restrict__ dist,
                           int* __restrict__ pick, float* __restrict__ xq) {
@@ -630,6 +713,9 @@ class GradImpl {
     const size_t asm_b = size_t(4) * T * (d / nh) * 4 + size_t(T) * T * 4;
     GCK(cudaFuncSetAttribute(kg_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_f)));
     GCK(cudaFuncSetAttribute(kg_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_b)));
+    if (kg_vq_tiled_smem(d) <= 200 * 1024)
+      GCK(cudaFuncSetAttribute(kg_vq_fwd_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(kg_vq_tiled_smem(d))));
     const int athreads = ((T + 31) / 32) * 32;
 
     // ---------------- forward
@@ -651,8 +737,13 @@ class GradImpl {
       gemm(false, false, R, d3, d, h1b, d, wqkv[b], d3, qb, d3, 0.f);
       kg_add_bias<<<ew(R * d3), 256, 0, st>>>(R, d3, qb, bqkv[b]);
       kg_attn_fwd<<<B * nh, athreads, asm_f, st>>>(T, d, nh, sc, qb, Pb, ab);
-      kg_vq_fwd<<<rowGrid, 256, 0, st>>>(R, d, Q, ab, W[pidx(b, 10)], db,
-                                         pick.p + size_t(b) * R, xqb);
+      if (kg_vq_tiled_smem(d) <= 200 * 1024) {
+        kg_vq_fwd_tiled<<<int((R + KGVQ_ROWS - 1) / KGVQ_ROWS), 256, kg_vq_tiled_smem(d), st>>>(
+            R, d, Q, ab, W[pidx(b, 10)], db, pick.p + size_t(b) * R, xqb);
+      } else {
+        kg_vq_fwd<<<rowGrid, 256, 0, st>>>(R, d, Q, ab, W[pidx(b, 10)], db,
+                                           pick.p + size_t(b) * R, xqb);
+      }
       // x1 = x + (xq Wo + bo)
       gemm(false, false, R, d, d, xqb, d, W[pidx(b, 8)], d, tmp.p, d, 0.f);
       kg_add3<<<ew(R * d), 256, 0, st>>>(R, d, xb, tmp.p, W[pidx(b, 9)], x1b);
