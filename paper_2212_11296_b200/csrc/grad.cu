@@ -214,45 +214,57 @@ __global__ void kg_gelu_bwd(int64_t n, const float* __restrict__ pre, float* __r
 
 // causal attention forward per (sample, head) (autodiff.cpp:336-379): the
 // probabilities are kept for the backward. One CTA of T threads, thread = row.
+// Shared-memory layouts are padded (row stride dh + 1, T + 1) so the
+// thread-per-query-row loops are bank-conflict free, and the probability tile
+// is built in shared memory and stored row-major with coalesced writes. The
+// arithmetic (every sum and its order) is that of the straightforward
+// per-row loops.
 __global__ void kg_attn_fwd(int T, int d, int nh, float sc, const float* __restrict__ qkv,
                             float* __restrict__ P, float* __restrict__ att) {
   extern __shared__ float sm[];
-  const int dh = d / nh;
+  const int dh = d / nh, dp = dh + 1, tp = T + 1;
   const int b = blockIdx.x / nh, h = blockIdx.x % nh;
   float* qs = sm;
-  float* ks = qs + T * dh;
-  float* vs = ks + T * dh;
+  float* ks = qs + T * dp;
+  float* vs = ks + T * dp;
+  float* Ps = vs + T * dp;  // Ps[j * tp + r] = P[r][j]
   for (int i = threadIdx.x; i < T * dh; i += blockDim.x) {
     const int r = i / dh, c = i % dh;
     const float* row = qkv + ((int64_t)b * T + r) * 3 * d + h * dh + c;
-    qs[i] = row[0];
-    ks[i] = row[d];
-    vs[i] = row[2 * d];
+    qs[r * dp + c] = row[0];
+    ks[r * dp + c] = row[d];
+    vs[r * dp + c] = row[2 * d];
   }
   __syncthreads();
   const int r = threadIdx.x;
-  if (r >= T) return;
-  float* pr = P + ((int64_t)blockIdx.x * T + r) * T;
-  float mx = -INFINITY;
-  for (int j = 0; j <= r; ++j) {
-    float s = 0.f;
-    for (int c = 0; c < dh; ++c) s = fmaf(qs[r * dh + c], ks[j * dh + c], s);
-    s *= sc;
-    pr[j] = s;
-    mx = fmaxf(mx, s);
+  if (r < T) {
+    float mx = -INFINITY;
+    for (int j = 0; j <= r; ++j) {
+      float s = 0.f;
+      for (int c = 0; c < dh; ++c) s = fmaf(qs[r * dp + c], ks[j * dp + c], s);
+      s *= sc;
+      Ps[j * tp + r] = s;
+      mx = fmaxf(mx, s);
+    }
+    float sum = 0.f;
+    for (int j = 0; j <= r; ++j) {
+      const float e = expf(Ps[j * tp + r] - mx);
+      Ps[j * tp + r] = e;
+      sum += e;
+    }
+    for (int j = 0; j <= r; ++j) Ps[j * tp + r] /= sum;
+    for (int j = r + 1; j < T; ++j) Ps[j * tp + r] = 0.f;
+    for (int c = 0; c < dh; ++c) {
+      float o = 0.f;
+      for (int j = 0; j <= r; ++j) o = fmaf(Ps[j * tp + r], vs[j * dp + c], o);
+      att[((int64_t)b * T + r) * d + h * dh + c] = o;
+    }
   }
-  float sum = 0.f;
-  for (int j = 0; j <= r; ++j) {
-    const float e = expf(pr[j] - mx);
-    pr[j] = e;
-    sum += e;
-  }
-  for (int j = 0; j <= r; ++j) pr[j] /= sum;
-  for (int j = r + 1; j < T; ++j) pr[j] = 0.f;
-  for (int c = 0; c < dh; ++c) {
-    float o = 0.f;
-    for (int j = 0; j <= r; ++j) o = fmaf(pr[j], vs[j * dh + c], o);
-    att[((int64_t)b * T + r) * d + h * dh + c] = o;
+  __syncthreads();
+  float* Pg = P + (int64_t)blockIdx.x * T * T;
+  for (int i = threadIdx.x; i < T * T; i += blockDim.x) {
+    const int rr = i / T, j = i % T;
+    Pg[i] = Ps[j * tp + rr];
   }
 }
 
@@ -263,50 +275,52 @@ __global__ void kg_attn_bwd(int T, int d, int nh, float sc, const float* __restr
                             const float* __restrict__ P, const float* __restrict__ dO,
                             float* __restrict__ dqkv) {
   extern __shared__ float sm[];
-  const int dh = d / nh;
+  const int dh = d / nh, dp = dh + 1, tp = T + 1;
   const int b = blockIdx.x / nh, h = blockIdx.x % nh;
   float* qs = sm;
-  float* ks = qs + T * dh;
-  float* vs = ks + T * dh;
-  float* gs = vs + T * dh;
-  float* dS = gs + T * dh;  // [T x T]
+  float* ks = qs + T * dp;
+  float* vs = ks + T * dp;
+  float* gs = vs + T * dp;
+  float* dS = gs + T * dp;  // dS[r * tp + j]
+  float* Ps = dS + T * tp;  // Ps[r * tp + j] = P[r][j]
   for (int i = threadIdx.x; i < T * dh; i += blockDim.x) {
     const int r = i / dh, c = i % dh;
     const int64_t row = (int64_t)b * T + r;
-    qs[i] = qkv[row * 3 * d + h * dh + c];
-    ks[i] = qkv[row * 3 * d + d + h * dh + c];
-    vs[i] = qkv[row * 3 * d + 2 * d + h * dh + c];
-    gs[i] = dO[row * d + h * dh + c];
+    qs[r * dp + c] = qkv[row * 3 * d + h * dh + c];
+    ks[r * dp + c] = qkv[row * 3 * d + d + h * dh + c];
+    vs[r * dp + c] = qkv[row * 3 * d + 2 * d + h * dh + c];
+    gs[r * dp + c] = dO[row * d + h * dh + c];
   }
+  const float* Pg = P + (int64_t)blockIdx.x * T * T;
+  for (int i = threadIdx.x; i < T * T; i += blockDim.x) Ps[(i / T) * tp + i % T] = Pg[i];
   __syncthreads();
   const int r = threadIdx.x;
-  const float* pr = P + ((int64_t)blockIdx.x * T + (r < T ? r : 0)) * T;
   if (r < T) {
+    const float* pr = Ps + r * tp;
     float dot = 0.f;
     for (int j = 0; j <= r; ++j) {
-      float dp = 0.f;
-      for (int c = 0; c < dh; ++c) dp = fmaf(gs[r * dh + c], vs[j * dh + c], dp);
-      dS[r * T + j] = dp;
-      dot += dp * pr[j];
+      float dpv = 0.f;
+      for (int c = 0; c < dh; ++c) dpv = fmaf(gs[r * dp + c], vs[j * dp + c], dpv);
+      dS[r * tp + j] = dpv;
+      dot += dpv * pr[j];
     }
-    for (int j = 0; j <= r; ++j) dS[r * T + j] = pr[j] * (dS[r * T + j] - dot);
-    for (int j = r + 1; j < T; ++j) dS[r * T + j] = 0.f;
+    for (int j = 0; j <= r; ++j) dS[r * tp + j] = pr[j] * (dS[r * tp + j] - dot);
+    for (int j = r + 1; j < T; ++j) dS[r * tp + j] = 0.f;
   }
   __syncthreads();
   if (r < T) {
     const int64_t row = (int64_t)b * T + r;
     for (int c = 0; c < dh; ++c) {
       float dq = 0.f;
-      for (int j = 0; j <= r; ++j) dq = fmaf(dS[r * T + j], ks[j * dh + c], dq);
+      for (int j = 0; j <= r; ++j) dq = fmaf(dS[r * tp + j], ks[j * dp + c], dq);
       dqkv[row * 3 * d + h * dh + c] = dq * sc;
     }
     // column r: dK_r = sum_i dS[i, r] Q_i sc, dV_r = sum_i P[i, r] dO_i
-    const float* Pb = P + (int64_t)blockIdx.x * T * T;
     for (int c = 0; c < dh; ++c) {
       float dk = 0.f, dv = 0.f;
       for (int i = r; i < T; ++i) {
-        dk = fmaf(dS[i * T + r], qs[i * dh + c], dk);
-        dv = fmaf(Pb[(int64_t)i * T + r], gs[i * dh + c], dv);
+        dk = fmaf(dS[i * tp + r], qs[i * dp + c], dk);
+        dv = fmaf(Ps[i * tp + r], gs[i * dp + c], dv);
       }
       dqkv[row * 3 * d + d + h * dh + c] = dk * sc;
       dqkv[row * 3 * d + 2 * d + h * dh + c] = dv;
@@ -709,8 +723,8 @@ class GradImpl {
     const int rowGrid = int((R + 7) / 8);
     auto ew = [&](int64_t n) { return int((n + 255) / 256); };
     const float sc = float(1.0 / std::sqrt(double(d / nh)));
-    const size_t asm_f = size_t(3) * T * (d / nh) * 4;
-    const size_t asm_b = size_t(4) * T * (d / nh) * 4 + size_t(T) * T * 4;
+    const size_t asm_f = (size_t(3) * T * (d / nh + 1) + size_t(T) * (T + 1)) * 4;
+    const size_t asm_b = (size_t(4) * T * (d / nh + 1) + 2 * size_t(T) * (T + 1)) * 4;
     GCK(cudaFuncSetAttribute(kg_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_f)));
     GCK(cudaFuncSetAttribute(kg_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_b)));
     if (kg_vq_tiled_smem(d) <= 200 * 1024)
