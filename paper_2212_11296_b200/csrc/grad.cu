@@ -214,6 +214,8 @@ __global__ void kg_gelu_bwd(int64_t n, const float* __restrict__ pre, float* __r
 
 // causal attention forward per (sample, head) (autodiff.cpp:336-379): the
 // probabilities are kept for the backward. One CTA of T threads, thread = row.
+constexpr int KG_REG_DH = 32;  // head width up to which a row lives in registers
+
 // Shared-memory layouts are padded (row stride dh + 1, T + 1) so the
 // thread-per-query-row loops are bank-conflict free, and the probability tile
 // is built in shared memory and stored row-major with coalesced writes. The
@@ -237,7 +239,43 @@ __global__ void kg_attn_fwd(int T, int d, int nh, float sc, const float* __restr
   }
   __syncthreads();
   const int r = threadIdx.x;
-  if (r < T) {
+  if (r < T && dh <= KG_REG_DH) {
+    // the row's q and its output accumulators in registers (each sum keeps
+    // its order: c ascending for a score, j ascending for an output)
+    float qr[KG_REG_DH], orow[KG_REG_DH];
+#pragma unroll
+    for (int c = 0; c < KG_REG_DH; ++c) {
+      qr[c] = c < dh ? qs[r * dp + c] : 0.f;
+      orow[c] = 0.f;
+    }
+    float mx = -INFINITY;
+    for (int j = 0; j <= r; ++j) {
+      float sv = 0.f;
+#pragma unroll
+      for (int c = 0; c < KG_REG_DH; ++c)
+        if (c < dh) sv = fmaf(qr[c], ks[j * dp + c], sv);
+      sv *= sc;
+      Ps[j * tp + r] = sv;
+      mx = fmaxf(mx, sv);
+    }
+    float sum = 0.f;
+    for (int j = 0; j <= r; ++j) {
+      const float e = expf(Ps[j * tp + r] - mx);
+      Ps[j * tp + r] = e;
+      sum += e;
+    }
+    for (int j = 0; j <= r; ++j) Ps[j * tp + r] /= sum;
+    for (int j = r + 1; j < T; ++j) Ps[j * tp + r] = 0.f;
+    for (int j = 0; j <= r; ++j) {
+      const float pj = Ps[j * tp + r];
+#pragma unroll
+      for (int c = 0; c < KG_REG_DH; ++c)
+        if (c < dh) orow[c] = fmaf(pj, vs[j * dp + c], orow[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < KG_REG_DH; ++c)
+      if (c < dh) att[((int64_t)b * T + r) * d + h * dh + c] = orow[c];
+  } else if (r < T) {
     float mx = -INFINITY;
     for (int j = 0; j <= r; ++j) {
       float s = 0.f;
@@ -295,7 +333,24 @@ __global__ void kg_attn_bwd(int T, int d, int nh, float sc, const float* __restr
   for (int i = threadIdx.x; i < T * T; i += blockDim.x) Ps[(i / T) * tp + i % T] = Pg[i];
   __syncthreads();
   const int r = threadIdx.x;
-  if (r < T) {
+  const bool regs = dh <= KG_REG_DH;
+  if (r < T && regs) {
+    const float* pr = Ps + r * tp;
+    float gr[KG_REG_DH];
+#pragma unroll
+    for (int c = 0; c < KG_REG_DH; ++c) gr[c] = c < dh ? gs[r * dp + c] : 0.f;
+    float dot = 0.f;
+    for (int j = 0; j <= r; ++j) {
+      float dpv = 0.f;
+#pragma unroll
+      for (int c = 0; c < KG_REG_DH; ++c)
+        if (c < dh) dpv = fmaf(gr[c], vs[j * dp + c], dpv);
+      dS[r * tp + j] = dpv;
+      dot += dpv * pr[j];
+    }
+    for (int j = 0; j <= r; ++j) dS[r * tp + j] = pr[j] * (dS[r * tp + j] - dot);
+    for (int j = r + 1; j < T; ++j) dS[r * tp + j] = 0.f;
+  } else if (r < T) {
     const float* pr = Ps + r * tp;
     float dot = 0.f;
     for (int j = 0; j <= r; ++j) {
@@ -308,7 +363,43 @@ __global__ void kg_attn_bwd(int T, int d, int nh, float sc, const float* __restr
     for (int j = r + 1; j < T; ++j) dS[r * tp + j] = 0.f;
   }
   __syncthreads();
-  if (r < T) {
+  if (r < T && regs) {
+    // accumulators in registers, each sum in its original order
+    const int64_t row = (int64_t)b * T + r;
+    float acc[KG_REG_DH];
+#pragma unroll
+    for (int c = 0; c < KG_REG_DH; ++c) acc[c] = 0.f;
+    for (int j = 0; j <= r; ++j) {
+      const float sj = dS[r * tp + j];
+#pragma unroll
+      for (int c = 0; c < KG_REG_DH; ++c)
+        if (c < dh) acc[c] = fmaf(sj, ks[j * dp + c], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < KG_REG_DH; ++c)
+      if (c < dh) dqkv[row * 3 * d + h * dh + c] = acc[c] * sc;
+    float dv[KG_REG_DH];
+#pragma unroll
+    for (int c = 0; c < KG_REG_DH; ++c) {
+      acc[c] = 0.f;
+      dv[c] = 0.f;
+    }
+    for (int i = r; i < T; ++i) {
+      const float si = dS[i * tp + r], pi = Ps[i * tp + r];
+#pragma unroll
+      for (int c = 0; c < KG_REG_DH; ++c)
+        if (c < dh) {
+          acc[c] = fmaf(si, qs[i * dp + c], acc[c]);
+          dv[c] = fmaf(pi, gs[i * dp + c], dv[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < KG_REG_DH; ++c)
+      if (c < dh) {
+        dqkv[row * 3 * d + d + h * dh + c] = acc[c] * sc;
+        dqkv[row * 3 * d + 2 * d + h * dh + c] = dv[c];
+      }
+  } else if (r < T) {
     const int64_t row = (int64_t)b * T + r;
     for (int c = 0; c < dh; ++c) {
       float dq = 0.f;
