@@ -62,11 +62,17 @@ __device__ __forceinline__ uint64_t hash64(uint64_t x) {
   return x;
 }
 
-// Reference GELU (tanh form), proj/src/tensor.cpp:126-132.
+// Reference GELU (tanh form), proj/src/tensor.cpp:126-132, evaluated as
+// 0.5 v (1 + tanh u) = v / (1 + e^{-2u}): one ex2 and one reciprocal on the
+// MUFU unit instead of tanhf (which made the W1 GEMM's epilogue, not its
+// MMAs, the bottleneck), and no cancellation in 1 + tanh u for u << 0
+// (relative error a few ulp everywhere; e^{-2u} = inf gives -0).
 __device__ __forceinline__ float gelu_f(float v) {
   const float c = 0.7978845608028654f;
   const float u = c * (v + 0.044715f * v * v * v);
-  return 0.5f * v * (1.0f + tanhf(u));
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-2.8853900817779268f * u));  // e^{-2u}
+  return __fdividef(v, 1.0f + e);
 }
 
 }  // namespace vqb
