@@ -338,41 +338,51 @@ __global__ void __launch_bounds__(512) k_dedup(
       h = (h + 1) & (cap - 1);
     }
   }
-  if (tid == 0) run_s = 0;
   __syncthreads();
-  // phase 2: ids in first-occurrence order
-  for (int c0 = 0; c0 < M; c0 += nt) {
-    const int i = c0 + tid;
-    bool flag = false;
+  // phase 2: ids in first-occurrence order. Warp w owns the contiguous
+  // location segment [w L, (w + 1) L): it counts its first occurrences, one
+  // block scan of the warp counts gives each warp its first id, and the warp
+  // numbers its segment in order with ballots (two block barriers in all).
+  const int nw = nt >> 5;
+  const int L = (M + nw - 1) / nw;
+  const int seg0 = min(M, w * L), seg1 = min(M, seg0 + L);
+  int mine = 0;
+  for (int i0 = seg0; i0 < seg1; i0 += 32) {
+    const int i = i0 + lane;
+    const bool flag = i < seg1 && trep[tb + slot[base + i]] == i;
+    mine += __popc(__ballot_sync(0xffffffffu, flag));
+  }
+  if (lane == 0) wtot[w] = mine;
+  __syncthreads();
+  if (w == 0) {
+    int v = lane < nw ? wtot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane < nw) wtot[lane] = v;  // inclusive
+    if (lane == 31) run_s = v;      // total
+  }
+  __syncthreads();
+  int next = w > 0 ? wtot[w - 1] : 0;
+  for (int i0 = seg0; i0 < seg1; i0 += 32) {
+    const int i = i0 + lane;
     int64_t h = 0;
-    if (i < M) {
+    bool flag = false;
+    if (i < seg1) {
       h = slot[base + i];
       flag = trep[tb + h] == i;
     }
     const unsigned m = __ballot_sync(0xffffffffu, flag);
-    const int before = __popc(m & ((1u << lane) - 1u));
-    if (lane == 0) wtot[w] = __popc(m);
-    __syncthreads();
-    if (w == 0) {
-      int v = lane < (nt >> 5) ? wtot[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += y;
-      }
-      wtot[lane] = v;  // inclusive
-    }
-    __syncthreads();
-    const int run = run_s;
     if (flag) {
-      const int id = run + (w > 0 ? wtot[w - 1] : 0) + before;
+      const int id = next + __popc(m & ((1u << lane) - 1u));
       tuid[tb + h] = id;
       rep_of[base + id] = i;
     }
-    __syncthreads();
-    if (tid == 0) run_s = run + wtot[(nt >> 5) - 1];
-    __syncthreads();
+    next += __popc(m);
   }
+  __syncthreads();
   // phase 3: scatter ids to locations
   for (int i = tid; i < M; i += nt) I_out[base + i] = tuid[tb + slot[base + i]];
   if (tid == 0) Ucnt[s] = run_s;
