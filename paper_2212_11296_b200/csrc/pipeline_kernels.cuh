@@ -416,6 +416,8 @@ __global__ void k_embed(int d, int R1, int T, int g, int V, const int32_t* __res
   }
 }
 
+constexpr int LN_REG = 8;  // row elements per lane kept in registers (d <= 256)
+
 // kernels::layer_norm (proj/src/tensor.cpp:57-83): two-pass biased variance,
 // eps 1e-5, statistics in double; one warp per row over *Mp rows.
 template <typename TA>
@@ -427,6 +429,33 @@ __global__ void k_layernorm(const int64_t* __restrict__ Mp, int d, const float* 
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
     const float* xr = x + r * d;
+    if (d <= 32 * LN_REG) {
+      // the row read once into registers (element lane + 32 k); same sums
+      float xv[LN_REG];
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k) {
+        const int c = lane + 32 * k;
+        xv[k] = c < d ? xr[c] : 0.f;
+        if (c < d) s += xv[k];
+      }
+      const double mean = warp_sum(s) / d;
+      double v = 0.0;
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k)
+        if (lane + 32 * k < d) {
+          const double t = xv[k] - mean;
+          v += t * t;
+        }
+      const double var = warp_sum(v) / d;
+      const double rstd = 1.0 / sqrt(var + 1e-5);
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k) {
+        const int c = lane + 32 * k;
+        if (c < d) out[r * d + c] = from_f<TA>((float)((xv[k] - mean) * rstd * gam[c] + bet[c]));
+      }
+      continue;
+    }
     double s = 0.0;
     for (int c = lane; c < d; c += 32) s += xr[c];
     const double mean = warp_sum(s) / d;
@@ -460,6 +489,37 @@ __global__ void k_cont_ln(const int64_t* __restrict__ Mp, int d, const float* __
     const float* xr = x + g_res[r] * d;
     const float* pr = pwo + (int64_t)g_code[r] * d;
     float* yr = y + r * d;
+    if (d <= 32 * LN_REG) {
+      // y kept in registers between the passes; same sums
+      float yv[LN_REG];
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k) {
+        const int c = lane + 32 * k;
+        yv[k] = 0.f;
+        if (c < d) {
+          yv[k] = xr[c] + pr[c];
+          yr[c] = yv[k];
+          s += yv[k];
+        }
+      }
+      const double mean = warp_sum(s) / d;
+      double q = 0.0;
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k)
+        if (lane + 32 * k < d) {
+          const double t = yv[k] - mean;
+          q += t * t;
+        }
+      const double var = warp_sum(q) / d;
+      const double rstd = 1.0 / sqrt(var + 1e-5);
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k) {
+        const int c = lane + 32 * k;
+        if (c < d) out[r * d + c] = from_f<TA>((float)((yv[k] - mean) * rstd * gam[c] + bet[c]));
+      }
+      continue;
+    }
     double s = 0.0;
     for (int c = lane; c < d; c += 32) {
       const float v = xr[c] + pr[c];
