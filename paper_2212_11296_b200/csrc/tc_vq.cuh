@@ -367,36 +367,49 @@ __global__ void __launch_bounds__(256) k_vq_rescore(
     const int32_t* __restrict__ ncand, const int32_t* __restrict__ cand,
     const bf16* __restrict__ xh, const bf16* __restrict__ xl, const float* __restrict__ cb32,
     int d, int Q, int32_t* __restrict__ code, unsigned long long* __restrict__ n_rescored) {
-  const int lane = threadIdx.x & 31;
+  // eight lanes per queued row, four rows per warp (a row has ~2 survivors:
+  // a lane per survivor left most of a 32-lane warp idle); each distance is
+  // one lane's sequential double sum as before
+  const int lane = threadIdx.x & 31, grp = lane >> 3, sub = lane & 7;
   const int nq = (int)*qcount;
   unsigned long long done = 0;
-  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nq;
-       k += (gridDim.x * blockDim.x) >> 5) {
-    const int64_t row = qrows[k];
-    const int n = ncand[row];
-    const bf16* xhr = xh + row * d;
-    const bf16* xlr = xl + row * d;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t k0 = wid * 4; k0 < nq; k0 += nwarps * 4) {
+    const int64_t k = k0 + grp;
+    const bool valid = k < nq;
     double best = INFINITY;
     int jb = 0x7fffffff;
-    if (n >= 0) {
-      if (lane < n) {
-        jb = cand[row * TCV_QCAND + lane];
-        best = vq_exact_d2(xhr, xlr, cb32 + (int64_t)jb * d, d);
-      }
-      done += n;
-    } else {
-#pragma unroll 1
-      for (int j = lane; j < Q; j += 32) {
-        const double s2 = vq_exact_d2(xhr, xlr, cb32 + (int64_t)j * d, d);
-        if (s2 < best) {  // j ascending per lane: strict < keeps the lowest index
-          best = s2;
-          jb = j;
+    int64_t row = 0;
+    if (valid) {
+      row = qrows[k];
+      const int n = ncand[row];
+      const bf16* xhr = xh + row * d;
+      const bf16* xlr = xl + row * d;
+      if (n >= 0) {
+        for (int t = sub; t < n; t += 8) {
+          const int j = cand[row * TCV_QCAND + t];
+          const double s2 = vq_exact_d2(xhr, xlr, cb32 + (int64_t)j * d, d);
+          if (s2 < best || (s2 == best && j < jb)) {
+            best = s2;
+            jb = j;
+          }
         }
+        if (sub == 0) done += n;
+      } else {
+#pragma unroll 1
+        for (int j = sub; j < Q; j += 8) {
+          const double s2 = vq_exact_d2(xhr, xlr, cb32 + (int64_t)j * d, d);
+          if (s2 < best) {  // j ascending per lane: strict < keeps the lowest index
+            best = s2;
+            jb = j;
+          }
+        }
+        if (sub == 0) done += Q;
       }
-      done += Q;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 4; o > 0; o >>= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, best, o);
       const int oj = __shfl_xor_sync(0xffffffffu, jb, o);
       if (ob < best || (ob == best && oj < jb)) {
@@ -406,9 +419,9 @@ __global__ void __launch_bounds__(256) k_vq_rescore(
     }
     // no finite distance (x or the codebook not finite): the reference's
     // argmin keeps its initial index 0 (proj/src/model.cpp:283-319)
-    if (lane == 0) code[row] = jb == 0x7fffffff ? 0 : jb;
+    if (valid && sub == 0) code[row] = jb == 0x7fffffff ? 0 : jb;
   }
-  if (n_rescored && lane == 0 && done) atomicAdd(n_rescored, done);
+  if (n_rescored && sub == 0 && done) atomicAdd(n_rescored, done);
 }
 
 // queue storage for the deferred re-scoring (device buffers, grown on demand)
