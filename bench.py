@@ -403,7 +403,7 @@ def main():
         "dedup_savings": {"total": tot_s, "quantized_ops": q_s,
                           "ledger": led.as_array().tolist()},
         "e2e": {"value": evals * ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(B * w.n_sites),
-                "d2h_bytes_per_step": int(3 * B * 8)},
+                "d2h_bytes_per_step": int(2 * B * 8)},
         "gpu_launches": int(launches_per_step * args.steps),
         "no_reuse": dense,
         "sampler": sampler,

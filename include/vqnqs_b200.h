@@ -143,6 +143,12 @@ int vqnqs_grad_destroy(vqnqs_grad_handle* h);
  * (proj/src/bench.cpp:193) and as an independent self-check. */
 int vqnqs_gpu_set_reuse(vqnqs_handle* h, int reuse);
 
+/* Samples per micro-batch ("chunk"). 0 (default) sizes it
+ * from a device working-set budget. Results do not depend on it (no
+ * reduction mixes samples); it exists for memory control and for the
+ * multi-micro-batch parity tests. */
+int vqnqs_gpu_set_micro_batch(vqnqs_handle* h, int samples);
+
 /* Replaces local_energies(model, h, batch, ledger)
  * (proj/include/vqnqs/trainer.hpp:76-79, proj/src/trainer.cpp:150-180).
  * configs: host [B x n_sites] bytes (0 = down, 1 = up). Outputs host arrays

@@ -14,6 +14,13 @@ int vqnqs_debug_gemm_bf16(int64_t M, int N, int K, const void* A, const void* WT
 /* code[M] = argmin_j |x_m - cb_j|^2 (fp32 x [M x d], fp32 cb [Q x d]). */
 int vqnqs_debug_vq(int64_t M, int d, const float* x, const float* cb32, int Q, int32_t* code,
                    int use_tc, unsigned long long* n_rescored);
+/* The tcgen05 gathered causal attention over an explicit location layout
+ * (see csrc/debug_hooks.cuh for the arrays); x = xh + xl per location. */
+int vqnqs_debug_tc_attention(int S, int R1, int T, int d, int nh, const int32_t* K,
+                             const int32_t* row_t1, const int32_t* row_perm,
+                             const int64_t* row_aoff, const int64_t* act_off, int64_t M,
+                             const int32_t* I, const int64_t* Uoff, const void* qkv, void* xh,
+                             void* xl, float* xn2, float* rr2);
 #ifdef __cplusplus
 }
 #endif

@@ -50,6 +50,7 @@ SIGNATURES = {
                                    C.c_int, C.POINTER(C.c_void_p)]),
     "vqnqs_gpu_set_hamiltonian": (C.c_int, [C.c_void_p, P_I32, C.c_int, C.c_int, C.c_int]),
     "vqnqs_gpu_set_reuse": (C.c_int, [C.c_void_p, C.c_int]),
+    "vqnqs_gpu_set_micro_batch": (C.c_int, [C.c_void_p, C.c_int]),
     "vqnqs_grad_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "vqnqs_grad_log_prob": (C.c_int, [C.c_void_p, P_U8, C.c_int64, P_F64, C.c_double, P_F64,
                                       P_F64]),

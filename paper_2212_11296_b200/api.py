@@ -326,6 +326,10 @@ class LocalEnergyEngine:
         location computed."""
         N.check(N.lib().vqnqs_gpu_set_reuse(self._h, int(bool(reuse))))
 
+    def set_micro_batch(self, samples: int) -> None:
+        """Samples per micro-batch (0 = sized from the working-set budget)."""
+        N.check(N.lib().vqnqs_gpu_set_micro_batch(self._h, int(samples)))
+
     def last_launch_count(self) -> int:
         return int(N.lib().vqnqs_gpu_last_launch_count(self._h))
 
@@ -335,22 +339,46 @@ class LocalEnergyEngine:
         return out
 
 
-_ENGINES: Dict[Tuple[int, int, str, int], LocalEnergyEngine] = {}
+def _fingerprint(model: VqTransformer, h: HamiltonianModel) -> bytes:
+    """Content hash of everything the engine snapshots at upload: the
+    weights, the config, the bonds and the Hamiltonian's options."""
+    import hashlib
+    m = hashlib.blake2b(digest_size=16)
+    m.update(repr(model.cfg).encode())
+    for p in model.params:
+        m.update(np.ascontiguousarray(p.value, np.float64).tobytes())
+    m.update(np.ascontiguousarray(h.lattice.bonds, np.int32).tobytes())
+    m.update(repr((h.kind, h.marshall, h.J, h.Gamma, h.n_sites())).encode())
+    return m.digest()
+
+
+# One cached engine for the stateless module-level calls. It is keyed on the
+# CONTENT of the model and Hamiltonian (not on id()), so a VMC loop that
+# updates parameters in place gets a fresh upload instead of stale weights,
+# and a single slot bounds the device memory it holds. Callers that evaluate
+# one model many times should hold a LocalEnergyEngine themselves: hashing
+# the weights costs a pass over them per call.
+_CACHE: Dict[str, object] = {}
 
 
 def _engine_for(model, h, precision, device) -> LocalEnergyEngine:
-    key = (id(model), id(h), precision, device)
-    eng = _ENGINES.get(key)
-    if eng is None:
-        eng = LocalEnergyEngine(model, h, precision, device)
-        _ENGINES[key] = eng
-    return eng
+    key = (_fingerprint(model, h), precision, device)
+    if _CACHE.get("key") != key:
+        old = _CACHE.pop("engine", None)
+        if old is not None:
+            old.close()
+        _CACHE["engine"] = LocalEnergyEngine(model, h, precision, device)
+        _CACHE["key"] = key
+    return _CACHE["engine"]
 
 
 def local_energies(model: VqTransformer, h: HamiltonianModel, batch,
                    ledger: Optional[Ledger] = None, precision: str = "fp32",
                    device: int = 0) -> np.ndarray:
-    """local_energies(model, h, batch, ledger) — complex E_loc per sample."""
+    """local_energies(model, h, batch, ledger) — complex E_loc per sample.
+
+    Stateless like the reference: every call evaluates the model's CURRENT
+    weights (the upload is cached on a content hash of model and h)."""
     e, _ = _engine_for(model, h, precision, device).local_energies(batch, ledger)
     return e
 

@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps.append(os.path.join(ROOT, "include", "vqnqs_b200.h"))
     if not force and _newer(LIB, deps):
         return LIB
-    objs = []
+    cmds, objs = [], []
     for src in SOURCES:
         obj = os.path.join(LIBDIR, src + ".o")
         cmd = [nvcc(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
@@ -55,8 +55,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd[1:1] = ["-x", "cu"] if False else []
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
+        cmds.append(cmd)
         objs.append(obj)
+    # the translation units compile in parallel (engine.cu dominates)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(len(cmds)) as ex:
+        for r in ex.map(lambda c: subprocess.run(c, check=True), cmds):
+            pass
     tmp = LIB + ".tmp"
     subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcublas"],
                    check=True)

@@ -156,6 +156,14 @@ int vqnqs_gpu_set_reuse(vqnqs_handle* h, int reuse) {
   });
 }
 
+int vqnqs_gpu_set_micro_batch(vqnqs_handle* h, int samples) {
+  return guarded([&] {
+    if (!h) throw vqb::UsageError("null handle");
+    if (samples < 0) throw vqb::ConfigError("micro-batch size must be >= 0");
+    h->eng->set_micro_batch(samples);
+  });
+}
+
 int vqnqs_gpu_local_energies(vqnqs_handle* h, const uint8_t* configs, int64_t B, double* e_re,
                              double* e_im, double* logpsi, int64_t* ledger7) {
   return guarded([&] {

@@ -5,6 +5,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
 #define VQB_EMPTY_KEY 0xFFFFFFFFFFFFFFFFull
 #define VQB_INT_MAX 0x7FFFFFFF
 
@@ -73,6 +79,37 @@ __device__ __forceinline__ float gelu_f(float v) {
   float e;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-2.8853900817779268f * u));  // e^{-2u}
   return __fdividef(v, 1.0f + e);
+}
+
+// Dynamic shared-memory opt-in for `fn` on the CURRENT device. The attribute
+// is a per-device setting, so it is tracked per (kernel, device): a process
+// that drives several GPUs (one host thread per device) opts in on each of
+// them. Thread-safe; a failure throws instead of surfacing later as a launch
+// error.
+inline void smem_optin(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) throw std::runtime_error("cudaGetDevice failed");
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{fn, dev}];
+  if (have >= bytes) return;
+  const cudaError_t e =
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e != cudaSuccess)
+    throw std::runtime_error("shared-memory opt-in of " + std::to_string(bytes) +
+                             " bytes failed: " + cudaGetErrorString(e));
+  have = bytes;
+}
+
+// Largest dynamic shared memory one CTA may opt in to on the current device.
+inline size_t smem_optin_limit() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return 227 * 1024;
+  return size_t(v);
 }
 
 }  // namespace vqb

@@ -50,20 +50,9 @@ extern "C" int vqnqs_debug_vq(int64_t M, int d, const float* x, const float* cb3
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   std::vector<float> h(size_t(Q) * d);
   cudaMemcpy(h.data(), cb32, h.size() * 4, cudaMemcpyDeviceToHost);
-  std::vector<float> wn2(Q);
-  std::vector<uint16_t> hb(h.size());
-  double wmax = 0;
-  for (int j = 0; j < Q; ++j) {
-    double a = 0;
-    for (int c = 0; c < d; ++c) a += double(h[size_t(j) * d + c]) * h[size_t(j) * d + c];
-    wn2[j] = float(a);
-    wmax = std::max(wmax, std::sqrt(a));
-  }
-  for (size_t i = 0; i < h.size(); ++i) {
-    uint32_t u;
-    std::memcpy(&u, &h[i], 4);
-    hb[i] = uint16_t(u >> 16);  // cb assumed bf16-exact
-  }
+  const VqCodebook pc = prepare_codebook(h.data(), Q, d);
+  const std::vector<float>& wn2 = pc.wn2;
+  const std::vector<uint16_t>& hb = pc.bf;
   float* dwn2 = nullptr;
   void* dcb = nullptr;
   cudaMalloc(&dwn2, Q * 4);
@@ -80,7 +69,7 @@ extern "C" int vqnqs_debug_vq(int64_t M, int d, const float* x, const float* cb3
     k_vq_prep<<<sms * 4, 256>>>(dM, d, x, xh, xl, xn2, rr2);
     const CUtensorMap tmB = make_tmap_bf16(dcb, uint64_t(Q), uint64_t(d), 256);
     VqScratch vqs;
-    tc_vq(dM, M, d, xh, xl, xn2, rr2, tmB, cb32, dwn2, float(wmax * (1 + 1e-6)), Q, code,
+    tc_vq(dM, M, d, xh, xl, xn2, rr2, tmB, cb32, dwn2, float(pc.wmax), float(pc.werr), Q, code,
           n_rescored, vqs, 0, sms);
     cudaDeviceSynchronize();
     vqs.release();
@@ -92,10 +81,10 @@ extern "C" int vqnqs_debug_vq(int64_t M, int d, const float* x, const float* cb3
     const int LOCS = d > 384 ? 32 : 64;
     const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;
     if (LOCS == 64) {
-      cudaFuncSetAttribute(k_vq<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(vsmem));
+      smem_optin(reinterpret_cast<const void*>(k_vq<64>), vsmem);
       k_vq<64><<<sms * 4, 256, vsmem>>>(dM, d, x, cb32, Q, code);
     } else {
-      cudaFuncSetAttribute(k_vq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(vsmem));
+      smem_optin(reinterpret_cast<const void*>(k_vq<32>), vsmem);
       k_vq<32><<<sms * 4, 256, vsmem>>>(dM, d, x, cb32, Q, code);
     }
   }
@@ -108,5 +97,69 @@ extern "C" int vqnqs_debug_vq(int64_t M, int d, const float* x, const float* cb3
   cudaFree(dM);
   cudaFree(dwn2);
   cudaFree(dcb);
+  return e == cudaSuccess ? 0 : 6;
+}
+
+// The tcgen05 gathered causal attention (k_tc_attention) on an explicit
+// location layout, with the same tile packing and per-layer tile tables the
+// engine builds (k_build_tiles, k_tile_info). Device pointers:
+//   K[S], row_t1[S*R1] (first changed token, -1 for the base row),
+//   row_perm[S*R1] (active-layout row order), row_aoff[S*R1] (layout offset
+//   of a row's first active location within its sample), act_off[S],
+//   I[M] (location -> sample-local unique row), Uoff[S], qkv [U x 3d] bf16.
+// Outputs: xh, xl [M x d] bf16 (x = xh + xl), xn2 [M], rr2 [M].
+extern "C" int vqnqs_debug_tc_attention(int S, int R1, int T, int d, int nh, const int32_t* K,
+                                        const int32_t* row_t1, const int32_t* row_perm,
+                                        const int64_t* row_aoff, const int64_t* act_off,
+                                        int64_t M, const int32_t* I, const int64_t* Uoff,
+                                        const void* qkv, void* xh, void* xl, float* xn2,
+                                        float* rr2) {
+  const int dh = d / nh;
+  if (!tc_attn_ok(1, d, dh, T)) return 3;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t R = int64_t(S) * R1;
+  int32_t *lrow = nullptr, *tcnt = nullptr, *ntiles = nullptr;
+  int16_t* lpos = nullptr;
+  int64_t *toff = nullptr, *dM = nullptr;
+  AttnTile* tiles = nullptr;
+  uint8_t* tinfo = nullptr;
+  const int64_t tcap = R + 16;
+  cudaMalloc(&lrow, M * 4);
+  cudaMalloc(&lpos, M * 2);
+  cudaMalloc(&tcnt, S * 4);
+  cudaMalloc(&ntiles, 4);
+  cudaMalloc(&toff, (S + 1) * 8);
+  cudaMalloc(&dM, 8);
+  cudaMalloc(&tiles, R * sizeof(AttnTile));
+  cudaMalloc(&tinfo, tcap * TINFO_BYTES);
+  cudaMemcpy(dM, &M, 8, cudaMemcpyHostToDevice);
+  k_enumerate<<<int((R * T + 255) / 256), 256>>>(S, R1, T, K, row_t1, row_aoff, act_off, lrow,
+                                                 lpos);
+  k_build_tiles<<<(S + 127) / 128, 128>>>(0, S, R1, T, K, row_t1, row_perm, act_off, tcnt,
+                                          nullptr, nullptr, tiles, ntiles);
+  k_scan<<<1, 1024>>>(S, tcnt, toff, toff + S, 0);
+  k_build_tiles<<<(S + 127) / 128, 128>>>(1, S, R1, T, K, row_t1, row_perm, act_off, tcnt, toff,
+                                          toff + S, tiles, ntiles);
+  k_tile_info<<<sms * 8, 128>>>(tiles, ntiles, R1, T, row_t1, act_off, lrow, lpos, I, Uoff,
+                                tinfo);
+  const size_t asmem = AttnSmem(T).total + 1024;
+  smem_optin(reinterpret_cast<const void*>(k_tc_attention), asmem);
+  k_tc_attention<<<sms, TCA_THREADS, asmem>>>(tinfo, ntiles, T, d, dh,
+                                              float(1.0 / std::sqrt(double(dh))),
+                                              static_cast<const bf16*>(qkv),
+                                              static_cast<bf16*>(xh), static_cast<bf16*>(xl),
+                                              xn2, rr2);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) fprintf(stderr, "vqnqs_debug_tc_attention: %s\n", cudaGetErrorString(e));
+  cudaFree(lrow);
+  cudaFree(lpos);
+  cudaFree(tcnt);
+  cudaFree(ntiles);
+  cudaFree(toff);
+  cudaFree(dM);
+  cudaFree(tiles);
+  cudaFree(tinfo);
   return e == cudaSuccess ? 0 : 6;
 }

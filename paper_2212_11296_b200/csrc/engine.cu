@@ -73,7 +73,7 @@ struct DBuf {
 struct DevBlock {
   float *ln1_g, *ln1_b, *bqkv, *bo, *ln2_g, *ln2_b, *b1, *b2, *cb32, *wn2;
   float* pwo;  // per-code continuation table [Q x d]: code_j Wo + bo
-  float wmax;
+  float wmax, werr;
   CUtensorMap tmB;                       // codebook tensor map (tcgen05 VQ)
   void *wqkv, *wo, *w1, *w2, *cbA;       // [in x out] row-major, operand type
   void *wqkvT, *woT, *w1T, *w2T;         // [out x in] (K-major) copies for tcgen05
@@ -277,19 +277,15 @@ class EngineImpl {
       B.wo = upload_op(std::vector<double>(wo, wo + (size_t)d * d));
       B.bo = upload_f(bo, d);
       B.cb32 = upload_f(cb, (int64_t)Q * d);
-      B.cbA = upload_op(std::vector<double>(cb, cb + (size_t)Q * d));
       {
-        // |W_j|^2 and max_j |W_j| for the certified argmin (tc_vq.cuh)
-        std::vector<float> wn2(Q);
-        double wmax = 0;
-        for (int j = 0; j < Q; ++j) {
-          double a = 0;
-          for (int cc = 0; cc < d; ++cc) a += cb[(size_t)j * d + cc] * cb[(size_t)j * d + cc];
-          wn2[j] = float(a);
-          wmax = std::max(wmax, std::sqrt(a));
-        }
-        B.wn2 = upload(wn2);
-        B.wmax = float(wmax * (1.0 + 1e-6));
+        // bf16 operand copy, |W_j|^2, max |W_j| and the bf16 rounding error
+        // of the codebook for the certified argmin (tc_vq.cuh)
+        const VqCodebook pc = prepare_codebook(cb, Q, d);
+        B.wn2 = upload(pc.wn2);
+        B.wmax = float(pc.wmax);
+        B.werr = float(pc.werr);
+        if (prec == VQNQS_PREC_BF16) B.cbA = upload(pc.bf);
+        else B.cbA = upload_op(std::vector<double>(cb, cb + (size_t)Q * d));
         if (use_tc_vq) B.tmB = make_tmap_bf16(B.cbA, uint64_t(Q), uint64_t(d), 256);
       }
       B.ln2_g = upload_f(ln2g, d);
@@ -372,7 +368,16 @@ class EngineImpl {
   }
 
   bool dense = false;  // no-reuse regime
+  int fixed_chunk = 0;  // set_micro_batch: fixed samples per micro-batch (0 = auto)
+  void set_micro_batch(int samples) {
+    fixed_chunk = samples;
+    size_chunks();
+  }
   void size_chunks() {
+    if (fixed_chunk > 0) {
+      S_max = fixed_chunk;
+      return;
+    }
     // micro-batch size: keep the per-location working set near a fixed budget.
     // ~ active locations per sample: a connected row (about half the bonds)
     // is active from its first changed token on, on average half the tokens;
@@ -397,6 +402,9 @@ class EngineImpl {
         throw ConfigError("bond " + std::to_string(b) + " out of range");
     }
     CK(cudaSetDevice(dev));
+    if (k_connected_smem(T, nbonds) > smem_optin_limit())
+      throw CapabilityError("GPU path: at most " +
+                            std::to_string(smem_optin_limit() / 32 - 1) + " bonds");
     if (d_bonds) cudaFree(d_bonds);
     d_bonds = nullptr;
     h_bonds.assign(bonds, bonds + 2 * nbonds);
@@ -444,7 +452,9 @@ class EngineImpl {
     row_bond_.ensure(R); row_perm_.ensure(R); row_t1_.ensure(R); row_aoff_.ensure(R); tok0_.ensure(int64_t(S) * T);
     Ucnt_.ensure(int64_t(L + 1) * S); Uoff_.ensure(int64_t(L + 1) * S); tot_.ensure(2 * (L + 2));
     int64_t* tot = tot_.p;  // [0] M total, [1] table total, [2+b] U_b total
-    k_connected<<<(S * 32 + 127) / 128, 128, 0, st>>>(S, N, g, T, nb, int(dense), d_cfg, d_bonds,
+    const size_t csmem = k_connected_smem(T, nb);
+    smem_optin(reinterpret_cast<const void*>(k_connected), csmem);
+    k_connected<<<(S * 32 + 127) / 128, 128, csmem, st>>>(S, N, g, T, nb, int(dense), d_cfg, d_bonds,
                                                       K_.p, diag_.p,
                                                       row_bond_.p, row_t1_.p, row_aoff_.p, Mact_.p,
                                                       tok0_.p, attw_.p, row_perm_.p);
@@ -529,20 +539,13 @@ class EngineImpl {
                                              lrow_.p, lpos_.p, Icur, Uo_cur, tinfo_.p);
         ++launches;
         const size_t asmem = AttnSmem(T).total + 1024;
-        static size_t attr = 0;
-        if (attr < asmem) {
-          CK(cudaFuncSetAttribute(k_tc_attention, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(asmem)));
-          attr = asmem;
-        }
+        smem_optin(reinterpret_cast<const void*>(k_tc_attention), asmem);
         k_tc_attention<<<sms, TCA_THREADS, asmem, st>>>(
             tinfo_.p, ntiles_.p, T, d, dh, scale, reinterpret_cast<const bf16*>(qkv), att_hi_.p,
             att_lo_.p, xn2_.p, rr2_.p);
       } else {
         const size_t asmem = (size_t(T) * (dh + 1) + size_t(T) * dh + 4 * T + 4 * dh) * 4;
-        if (asmem > 48 * 1024)
-          CK(cudaFuncSetAttribute(k_attention<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(asmem)));
+        smem_optin(reinterpret_cast<const void*>(k_attention<TA>), asmem);
         k_attention<TA><<<dim3(unsigned(R), nh), 128, asmem, st>>>(
             R1, T, d, dh, scale, K_.p, row_t1_.p, row_aoff_.p, act_off_.p, Icur, Uo_cur, qkv,
             att_.p);
@@ -555,7 +558,7 @@ class EngineImpl {
                                                rr2_.p);
             ++launches;
           }
-          tc_vq(tot + 0, M, d, att_hi_.p, att_lo_.p, xn2_.p, rr2_.p, B.tmB, B.cb32, B.wn2, B.wmax, Q,
+          tc_vq(tot + 0, M, d, att_hi_.p, att_lo_.p, xn2_.p, rr2_.p, B.tmB, B.cb32, B.wn2, B.wmax, B.werr, Q,
                 code_.p, d_rescored, vqs_, st, sms);
           ++launches;
         } else {
@@ -564,14 +567,10 @@ class EngineImpl {
           const int vgrid =
               int(std::max<int64_t>(1, std::min<int64_t>((M + LOCS - 1) / LOCS, sms * 4)));
           if (LOCS == 64) {
-            if (vsmem > 48 * 1024)
-              CK(cudaFuncSetAttribute(k_vq<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(vsmem)));
+            smem_optin(reinterpret_cast<const void*>(k_vq<64>), vsmem);
             k_vq<64><<<vgrid, 256, vsmem, st>>>(tot + 0, d, att_.p, B.cb32, Q, code_.p);
           } else {
-            if (vsmem > 48 * 1024)
-              CK(cudaFuncSetAttribute(k_vq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(vsmem)));
+            smem_optin(reinterpret_cast<const void*>(k_vq<32>), vsmem);
             k_vq<32><<<vgrid, 256, vsmem, st>>>(tot + 0, d, att_.p, B.cb32, Q, code_.p);
           }
         }
@@ -781,9 +780,7 @@ class EngineImpl {
     TA* fp = reinterpret_cast<TA*>(f1.p);
     const int awpb = 4;
     const size_t asmem = size_t(awpb) * (dh + T) * sizeof(float);
-    if (asmem > 48 * 1024)
-      CK(cudaFuncSetAttribute(k_dec_attention<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              int(asmem)));
+    smem_optin(reinterpret_cast<const void*>(k_dec_attention<TA>), asmem);
     launches += 2;
     for (int t = 0; t < T; ++t) {
       k_dec_embed<<<B, 128, 0, st>>>(B, d, T, V, t, d_tok, tok_embed, pos_embed, x.p);
@@ -804,7 +801,7 @@ class EngineImpl {
         launches += 2;
         if (use_tc_vq) {
           k_vq_prep<<<sms * 8, 256, 0, st>>>(dB.p, d, att.p, xh.p, xl.p, xn2.p, rr2.p);
-          tc_vq(dB.p, B, d, xh.p, xl.p, xn2.p, rr2.p, Bk.tmB, Bk.cb32, Bk.wn2, Bk.wmax, Q,
+          tc_vq(dB.p, B, d, xh.p, xl.p, xn2.p, rr2.p, Bk.tmB, Bk.cb32, Bk.wn2, Bk.wmax, Bk.werr, Q,
                 code.p, nullptr, vqs_, st, sms);
           launches += 3;
         } else {
@@ -813,14 +810,10 @@ class EngineImpl {
           const int vgrid = int(std::max<int64_t>(1, std::min<int64_t>((B + LOCS - 1) / LOCS,
                                                                         int64_t(sms) * 4)));
           if (LOCS == 64) {
-            if (vsmem > 48 * 1024)
-              CK(cudaFuncSetAttribute(k_vq<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(vsmem)));
+            smem_optin(reinterpret_cast<const void*>(k_vq<64>), vsmem);
             k_vq<64><<<vgrid, 256, vsmem, st>>>(dB.p, d, att.p, Bk.cb32, Q, code.p);
           } else {
-            if (vsmem > 48 * 1024)
-              CK(cudaFuncSetAttribute(k_vq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(vsmem)));
+            smem_optin(reinterpret_cast<const void*>(k_vq<32>), vsmem);
             k_vq<32><<<vgrid, 256, vsmem, st>>>(dB.p, d, att.p, Bk.cb32, Q, code.p);
           }
           ++launches;
@@ -926,6 +919,7 @@ Engine::Engine(const vqnqs_model_desc& d, const double* const* params, int n_par
     : p_(new EngineImpl(d, params, n_params, precision, device)) {}
 Engine::~Engine() { delete p_; }
 void Engine::set_reuse(bool reuse) { p_->set_reuse(reuse); }
+void Engine::set_micro_batch(int samples) { p_->set_micro_batch(samples); }
 void Engine::set_hamiltonian(const int32_t* bonds, int nb, int n_sites, bool marshall) {
   p_->set_hamiltonian(bonds, nb, n_sites, marshall);
 }

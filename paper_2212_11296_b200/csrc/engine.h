@@ -86,6 +86,8 @@ class Engine {
   // reuse = false: the no-reuse (dense) regime of proj/src/bench.cpp:19-36 —
   // every row active from position 0, every location its own unique row.
   void set_reuse(bool reuse);
+  // samples per micro-batch; 0 = sized from the working-set budget
+  void set_micro_batch(int samples);
 
   struct Taps {
     int32_t* K = nullptr;       // [B]

@@ -16,6 +16,8 @@
 // locations first, then each row's suffix in row order.
 #pragma once
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace vqb {
@@ -118,10 +120,12 @@ __global__ void k_connected(int S, int N, int g, int T, int nb, int dense,
   // suffix length, so attention tiles built in this order (row_perm) have
   // tight live score ranges. Values are unaffected: unique rows are
   // order-independent and U counts are order-invariant.
-  __shared__ int hist_all[4][1025];
-  __shared__ int sloc_all[4][1025];
-  int* hist = hist_all[(threadIdx.x >> 5) & 3];
-  int* sloc = sloc_all[(threadIdx.x >> 5) & 3];
+  // per-warp scratch of max(T, nb + 1) ints each (dynamic: a lattice may have
+  // more connected rows than tokens; k_connected_smem sizes it)
+  extern __shared__ int kc_smem[];
+  const int W = max(T, R1);
+  int* hist = kc_smem + ((threadIdx.x >> 5) & 3) * 2 * W;
+  int* sloc = hist + W;
   for (int t = lane; t < T; t += 32) hist[t] = 0;
   __syncwarp();
   const unsigned lt = (1u << lane) - 1u;
@@ -210,6 +214,11 @@ __global__ void k_connected(int S, int N, int g, int T, int nb, int dense,
     }
     for (int q = 0; q < nrows; ++q) row_perm[pb + q] = ord[q];
   }
+}
+
+// dynamic shared memory of a 128-thread k_connected block
+inline size_t k_connected_smem(int T, int nb) {
+  return size_t(4) * 2 * size_t(std::max(T, nb + 1)) * sizeof(int);
 }
 
 // Exclusive scan of per-sample counts (single CTA). mode 1 scans hash-table

@@ -4,7 +4,10 @@
 #include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
+#include <cmath>
+#include <cstring>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "tc_gemm.cuh"
@@ -16,19 +19,17 @@ namespace vqb {
 inline bool tc_gemm_ok(int prec, int N, int K) {
   return prec == 1 && K % 64 == 0 && N % 64 == 0;
 }
-inline bool tc_vq_ok(int prec, int d, int Q) { return prec == 1 && d % 64 == 0 && Q % 256 == 0; }
+// ... and the VQ kernel keeps all Q code norms resident in shared memory.
+inline bool tc_vq_ok(int prec, int d, int Q) {
+  return prec == 1 && d % 64 == 0 && Q % 256 == 0 && tcv_smem_bytes(Q) <= smem_optin_limit();
+}
 
 template <int BN, int EPI>
 inline void launch_tc_gemm_ws(const int64_t* Mp, int64_t Mcap, int N, int K, const bf16* A,
                               int lda, const bf16* WT, const float* bias, void* out, int ldo,
                               const float* resid, int ldr, cudaStream_t st, int sms) {
   const size_t smem = tcw_smem_bytes<BN>();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tc_gemm_ws<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_tc_gemm_ws<BN, EPI>), smem);
   const CUtensorMap tmA = make_tmap_bf16(A, uint64_t(Mcap), uint64_t(K), 128, uint64_t(lda));
   const CUtensorMap tmW = make_tmap_bf16(WT, uint64_t(N), uint64_t(K), BN);
   const int64_t tiles = ((Mcap + 127) / 128) * (N / BN);
@@ -99,25 +100,59 @@ __global__ void k_vq_prep(const int64_t* __restrict__ Mp, int d, const float* __
   }
 }
 
+// Host-side codebook preparation for tc_vq: the bf16 operand copy (round to
+// nearest), |W_j|^2 of the given codebook, max_j |W_j| and
+// max_j |W_j - bf16(W_j)| (the certified bound's two codebook terms).
+struct VqCodebook {
+  std::vector<uint16_t> bf;
+  std::vector<float> wn2;
+  double wmax = 0, werr = 0;
+};
+template <typename T>
+inline VqCodebook prepare_codebook(const T* cb, int Q, int d) {
+  VqCodebook o;
+  o.bf.resize(size_t(Q) * d);
+  o.wn2.resize(Q);
+  for (int j = 0; j < Q; ++j) {
+    double a = 0, e = 0;
+    for (int c = 0; c < d; ++c) {
+      const double w = double(cb[size_t(j) * d + c]);
+      a += w * w;
+      float f = float(w);
+      uint32_t u;
+      std::memcpy(&u, &f, 4);
+      if ((u & 0x7f800000u) != 0x7f800000u) u += 0x7fffu + ((u >> 16) & 1u);
+      const uint16_t b = uint16_t(u >> 16);
+      o.bf[size_t(j) * d + c] = b;
+      uint32_t ub = uint32_t(b) << 16;
+      float fb;
+      std::memcpy(&fb, &ub, 4);
+      e += (w - double(fb)) * (w - double(fb));
+    }
+    o.wn2[j] = float(a);
+    o.wmax = std::max(o.wmax, std::sqrt(a));
+    o.werr = std::max(o.werr, std::sqrt(e));
+  }
+  o.wmax *= 1.0 + 1e-6;
+  o.werr *= 1.0 + 1e-6;
+  return o;
+}
+
 // xh/xl: [Mcap x d] bf16 planes; tmB: the layer's codebook tensor map
 // (make_tmap_bf16(cbA, Q, d, 256)).
 inline void tc_vq(const int64_t* Mp, int64_t Mcap, int d, const bf16* xh, const bf16* xl,
                   const float* xn2, const float* xl2, const CUtensorMap& tmB, const float* cb32,
-                  const float* wn2, float wmax, int Q, int32_t* code,
+                  const float* wn2, float wmax, float werr, int Q, int32_t* code,
                   unsigned long long* n_rescored, VqScratch& q, cudaStream_t st, int sms) {
   const size_t smem = tcv_smem_bytes(Q);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaFuncSetAttribute(k_tc_vq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = smem;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_tc_vq), smem);
   q.ensure(size_t(Mcap));
   cudaMemsetAsync(q.qcount, 0, sizeof(uint32_t), st);
   const CUtensorMap tmA = make_tmap_bf16(xh, uint64_t(Mcap), uint64_t(d), 128);
   const CUtensorMap tmL = make_tmap_bf16(xl, uint64_t(Mcap), uint64_t(d), 128);
   const int64_t tiles = (Mcap + 127) / 128;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
-  k_tc_vq<<<grid, TCV_THREADS, smem, st>>>(tmA, tmL, tmB, Mp, d, xn2, xl2, wn2, wmax, Q, code,
+  k_tc_vq<<<grid, TCV_THREADS, smem, st>>>(tmA, tmL, tmB, Mp, d, xn2, xl2, wn2, wmax, werr, Q, code,
                                            q.cand, q.ncand, q.qrows, q.qcount);
   k_vq_rescore<<<sms * 2, 256, 0, st>>>(q.qcount, q.qrows, q.ncand, q.cand, xh, xl, cb32, d, Q,
                                         code, n_rescored);

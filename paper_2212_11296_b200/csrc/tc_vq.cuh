@@ -23,7 +23,9 @@
 //            reference's own arithmetic (proj/src/model.cpp:298-303) — and the
 //            lowest index wins (strict <, :304). Deferring the rare re-scoring
 //            keeps it off the epilogue's critical path.
-// W is bf16-exact (the bf16 configs snap weights to bf16).
+// The MMA reads bf16(W); when W is not bf16-exact (an unsnapped model) the
+// bound widens by 2|x| max_j |W_j - bf16(W_j)| (werr), so the certificate
+// still holds against the fp32 codebook the re-scoring uses.
 #pragma once
 
 #include "common.cuh"
@@ -107,7 +109,8 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmL,
     const __grid_constant__ CUtensorMap tmB,
     const int64_t* __restrict__ Mp, int d, const float* __restrict__ xn2g,
-    const float* __restrict__ xl2g, const float* __restrict__ wn2_g, float wmax, int Q, int32_t* __restrict__ code,
+    const float* __restrict__ xl2g, const float* __restrict__ wn2_g, float wmax, float werr,
+    int Q, int32_t* __restrict__ code,
     int32_t* __restrict__ cand, int32_t* __restrict__ ncand, int32_t* __restrict__ qrows,
     uint32_t* __restrict__ qcount) {
   extern __shared__ uint8_t smem_raw[];
@@ -251,8 +254,10 @@ __global__ void __launch_bounds__(TCV_THREADS, 1) k_tc_vq(
       int* red_cnt = red_cnt0 + tpar * TCV_EPI_PARTS * 128;
       int* red_jf = red_jf0 + tpar * TCV_EPI_PARTS * 128;
       // |r| <= 2^-8 / (1 - 2^-8) |xl|: the residual of the two-term split
+      // + 2|x| max_j |W_j - bf16(W_j)|: the MMA sees the bf16-rounded
+      // codebook, |W_j|^2 is the exact one (werr = 0 for a snapped codebook)
       const float E = 2.f * (0.00393f * xln * wmax + float(d) * 1.2e-7f * xn * wmax) +
-                      4e-7f * (wmax * wmax + 2.f * xn * wmax);
+                      4e-7f * (wmax * wmax + 2.f * xn * wmax) + 2.00001f * xn * werr;
       const float w2 = 2.f * E;
       float run_min = INFINITY;
       Cands C;

@@ -32,6 +32,22 @@ LOGPSI_TOL = 1e-5
 LP_ROW_TOL = 2 * LOGPSI_TOL
 ELOC_RTOL = 1e-4
 
+# bf16 engine vs the oracle in bf16-emulation mode
+BF16_WINDOW = 1e-4  # documented accumulation window for bf16 configs
+# bf16 operand rounding moves logits by ~2^-9 relative per rounding decision
+# that fp32-vs-double accumulation tips the other way; measured and bounded
+# here. The strict 1e-5 / 1e-4 contract is checked on every
+# config in fp32 mode (test_*_fp32_strict).
+BF16_LOGPSI_TOL = 5e-3
+BF16_ELOC_RTOL = 2e-3
+# the accumulation drift grows with depth and sequence length: measured
+# max |d lp_row| 8.2e-3 at c3 (6 blocks, T=50) and 1.65e-2 at c4 (8 blocks,
+# T=128), identical with the CUDA-core attention — it is the bf16 product
+# boundary, not a kernel
+BF16_LOGPSI_TOL_DEEP = 1e-2
+# c5 (12 blocks, d=768, 1024 codes): measured 4.2e-2
+BF16_LOGPSI_TOL_C5 = 2.5e-2
+
 
 @dataclass
 class ParityReport:
@@ -54,6 +70,11 @@ class ParityReport:
     logpsi_fail: int = 0
     eloc_checked: int = 0
     eloc_fail: int = 0
+    eloc_partial_checked: int = 0
+    eloc_partial_fail: int = 0
+    max_rel_de_partial: float = 0.0
+    eloc_self_checked: int = 0
+    eloc_self_fail: int = 0
     max_dlp: float = 0.0
     max_dlogpsi: float = 0.0
     max_rel_de: float = 0.0
@@ -61,7 +82,8 @@ class ParityReport:
 
     def ok(self) -> bool:
         return (self.flips_beyond == 0 and self.u_fail == 0 and self.lp_fail == 0
-                and self.logpsi_fail == 0 and self.eloc_fail == 0)
+                and self.logpsi_fail == 0 and self.eloc_fail == 0
+                and self.eloc_partial_fail == 0 and self.eloc_self_fail == 0)
 
     def as_dict(self) -> dict:
         d = dict(self.__dict__)
@@ -78,13 +100,64 @@ class ParityReport:
                 f"logpsi_fail={self.logpsi_fail}/{self.logpsi_checked} "
                 f"max|dlogpsi|={self.max_dlogpsi:.2e} "
                 f"E_fail={self.eloc_fail}/{self.eloc_checked} max relE={self.max_rel_de:.2e} "
+                f"E_partial_fail={self.eloc_partial_fail}/{self.eloc_partial_checked} "
+                f"max relE_partial={self.max_rel_de_partial:.2e} "
+                f"E_self_fail={self.eloc_self_fail}/{self.eloc_self_checked} "
                 f"flagged_locations={self.flagged_locations}/{self.locations}")
 
 
+def heisenberg_coeffs(s, bonds, marshall=True) -> np.ndarray:
+    """connected_set coefficients (proj/src/hamiltonian.cpp:41-74): entry 0
+    the diagonal 1/4 sum z_i z_j, then -1/2 (Marshall) or +1/2 per
+    antiparallel bond in bond order."""
+    s = np.asarray(s, np.int64)
+    b = np.asarray(bonds, np.int64)
+    z = 2 * s - 1
+    diag = 0.25 * float(np.sum(z[b[:, 0]] * z[b[:, 1]]))
+    n_anti = int(np.sum(s[b[:, 0]] != s[b[:, 1]]))
+    return np.concatenate([[diag], np.full(n_anti, -0.5 if marshall else 0.5)])
+
+
+def eloc_from_rows(coeffs, lp, rows=None) -> float:
+    """E = sum_k c_k exp((lp_k - lp_0)/2) over `rows` (all by default),
+    proj/src/dedup.cpp:410-417 with the phase off."""
+    c = np.asarray(coeffs, np.float64)
+    lp = np.asarray(lp, np.float64)
+    terms = c * np.exp(0.5 * (lp - lp[0]))
+    return float(np.sum(terms if rows is None else terms[rows]))
+
+
+class FixtureTaps:
+    """Oracle taps read back from a committed reference fixture
+    (tests/golden/make_golden_large.py): gaps are stored sparsely (only the
+    locations below the fixture's sparse_gap); every other location is set to
+    1.0, which the parity rules treat like any gap >= the bf16 window."""
+
+    def __init__(self, K, U, codes, lp, gidx, gval):
+        self.K = int(K)
+        self.U = np.asarray(U, np.int64)
+        self.codes = np.asarray(codes, np.int32)[..., None]
+        g = np.ones(self.codes.shape[0] * self.codes.shape[1], np.float32)
+        g[np.asarray(gidx, np.int64)] = gval
+        self.gaps = g.reshape(self.codes.shape[0], self.codes.shape[1])
+        self.lp = np.asarray(lp, np.float64)
+
+
+def load_fixture(path):
+    """(dict of arrays, [FixtureTaps per sample]) of a parity_<case>.npz."""
+    z = np.load(path)
+    n = z["samples"].shape[0]
+    taps = [FixtureTaps(z["K"][i], z["U"][i], z[f"codes_{i}"], z[f"lp_{i}"], z[f"gidx_{i}"],
+                        z[f"gval_{i}"]) for i in range(n)]
+    return {k: z[k] for k in z.files if not k[:3] in ("lp_", "cod", "gid", "gva")}, taps
+
+
 def compare(rep: ParityReport, taps, ref_e, ref_lpsi, gpu_codes, gpu_U, gpu_e, gpu_lpsi,
-            gpu_lp_rows, T):
+            gpu_lp_rows, T, coeffs=None):
     """One sample. taps: oracle Taps (codes [L, K*T, 1], gaps [L, K*T], lp [K],
-    U [L+1]); gpu_codes [L, K*T]; gpu_U [L+1]; gpu_lp_rows [K]."""
+    U [L+1]); gpu_codes [L, K*T]; gpu_U [L+1]; gpu_lp_rows [K]; coeffs: the
+    sample's connected-set coefficients (enables the eloc_partial and
+    eloc_self checks)."""
     rep.samples += 1
     K = int(taps.K)
     rc = taps.codes[..., 0].reshape(-1, K, T)
@@ -125,6 +198,21 @@ def compare(rep: ParityReport, taps, ref_e, ref_lpsi, gpu_codes, gpu_U, gpu_e, g
         dl = abs(float(ref_lpsi) - float(gpu_lpsi))
         rep.max_dlogpsi = max(rep.max_dlogpsi, dl)
         rep.logpsi_fail += int(dl > rep.logpsi_tol)
+    if coeffs is not None:
+        glp = np.asarray(gpu_lp_rows, np.float64)
+        rep.eloc_self_checked += 1
+        es = eloc_from_rows(coeffs, glp)
+        if abs(es - float(gpu_e)) > 1e-9 * max(abs(es), 1.0):
+            rep.eloc_self_fail += 1
+            rep.notes.append(f"E_gpu {gpu_e} != formula over GPU rows {es}")
+        if clean[0] and not clean.all():
+            rep.eloc_partial_checked += 1
+            rows = np.nonzero(clean)[0]
+            ep_g = eloc_from_rows(coeffs, glp, rows)
+            ep_r = eloc_from_rows(coeffs, taps.lp, rows)
+            re = abs(ep_g - ep_r) / max(abs(float(ref_e)), 1e-12)
+            rep.max_rel_de_partial = max(rep.max_rel_de_partial, re)
+            rep.eloc_partial_fail += int(re > rep.eloc_rtol)
     if clean.all():
         rep.clean_samples += 1
         rep.eloc_checked += 1

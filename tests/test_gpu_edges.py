@@ -15,7 +15,7 @@ import pytest
 
 import paper_2212_11296_b200 as P
 from parity import ParityReport, compare
-from test_gpu_parity import BF16_ELOC_RTOL, BF16_LOGPSI_TOL, BF16_WINDOW
+from parity import BF16_ELOC_RTOL, BF16_LOGPSI_TOL, BF16_WINDOW
 
 pytestmark = pytest.mark.gpu
 

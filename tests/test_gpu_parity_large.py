@@ -1,0 +1,136 @@
+"""GPU parity at the benchmarked workloads (c3, c4, c5) against fixtures the
+REFERENCE generated (tests/golden/make_golden_large.py: oracle/_ref, i.e.
+proj/src compiled unmodified, run on seeded samples of each workload in plain
+double and in bf16-emulation mode). The CPU reference needs ~110 s per c4
+sample and minutes per c5 sample, so these tests compare against the
+committed outputs instead of running it live; every case runs in the driver's
+`pytest -m gpu`.
+
+  fp32 engine vs the reference in double           : the north-star contract
+      (codes exact except at flagged gaps < 1e-5, unique-row counts exact up
+      to the first flip, logpsi 1e-5, E_loc 1e-4 relative);
+  bf16 engine vs the reference in bf16 emulation   : the documented bf16
+      accumulation window and tolerances (tests/test_gpu_parity.py,
+      DESIGN.md §5).
+
+Each test prints its ParityReport (how many code, U, logpsi and E_loc
+comparisons actually ran) and, with VQNQS_PARITY_REPORT=<file>, appends it as
+a JSON line.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2212_11296_b200 as P
+from parity import (BF16_ELOC_RTOL, BF16_LOGPSI_TOL, BF16_LOGPSI_TOL_C5, BF16_LOGPSI_TOL_DEEP,
+                    BF16_WINDOW, ParityReport, compare, heisenberg_coeffs, load_fixture)
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+_ENGINES = {}
+
+
+def engine(name, precision):
+    key = (name, precision)
+    if key not in _ENGINES:
+        w = P.workload(name)
+        model = P.VqTransformer.init(w.model, w.weight_seed, snap_bf16=precision == "bf16")
+        lat = P.build_lattice("grid2d", (w.L, w.L), periodic=True)
+        _ENGINES.clear()  # one resident model at a time (c5 is 85M parameters)
+        _ENGINES[key] = (w, lat, P.LocalEnergyEngine(model, P.HamiltonianModel(lat),
+                                                      precision=precision))
+    return _ENGINES[key]
+
+
+def check_case(case, precision, micro_batch=0, **tol):
+    z, taps = load_fixture(os.path.join(GOLDEN, f"parity_{case}.npz"))
+    w, lat, eng = engine(str(z["workload"]), precision)
+    eng.set_micro_batch(micro_batch)
+    S = z["samples"]
+    led = P.Ledger()
+    e, lpsi = eng.local_energies(S, led)
+    K, U, codes, lps = eng.taps(S)
+    # the taps pass reproduces the energy pass bit for bit
+    assert np.array_equal([0.5 * lp[0] for lp in lps], lpsi)
+    rep = ParityReport(**tol) if tol else ParityReport()
+    for i in range(S.shape[0]):
+        assert int(K[i]) == taps[i].K
+        compare(rep, taps[i], z["e_re"][i], z["logpsi"][i], codes[i], U[i], e[i].real, lpsi[i],
+                lps[i], w.model.seq_len, coeffs=heisenberg_coeffs(S[i], lat.bonds))
+    print(f"\n[{case} {precision} micro_batch={micro_batch}] {rep.summary()}")
+    out = os.environ.get("VQNQS_PARITY_REPORT")
+    if out:
+        with open(out, "a") as f:
+            f.write(json.dumps({"case": case, "precision": precision,
+                                "micro_batch": micro_batch, **rep.as_dict()}) + "\n")
+    assert rep.ok(), rep.summary() + "\n" + "\n".join(rep.notes[:10])
+    if rep.clean_samples == rep.samples:
+        assert np.array_equal(led.as_array(), z["ledger"])
+    return rep, e, lpsi
+
+
+# ---- the north-star contract: fp32 engine vs the reference in double ----
+
+def test_c3_fp32_strict():
+    rep, _, _ = check_case("c3_fp64", "fp32")
+    assert rep.logpsi_checked >= 0.75 * rep.samples
+    assert rep.eloc_checked + rep.eloc_partial_checked >= 0.75 * rep.samples
+
+
+def test_c4_fp32_strict():
+    rep, _, _ = check_case("c4_fp64", "fp32")
+    assert rep.logpsi_checked >= 0.75 * rep.samples
+    assert rep.eloc_checked + rep.eloc_partial_checked >= 0.75 * rep.samples
+
+
+def test_c5_fp32_strict():
+    rep, _, _ = check_case("c5_fp64", "fp32")
+    # c5's codebook (1024 codes, d = 768, init scale 1/d) is dense in
+    # near-ties: ~9% of locations have a top-2 gap < 1e-5, so most rows see a
+    # flagged flip; the base rows' logpsi and the clean rows' energies remain
+    assert rep.logpsi_checked >= 0.5 * rep.samples
+    assert rep.clean_rows >= 0.05 * rep.rows
+
+
+# ---- bf16 engine vs the reference in bf16 emulation ----
+
+BF16 = dict(window=BF16_WINDOW, eloc_rtol=BF16_ELOC_RTOL)
+
+
+def test_c3_bf16():
+    rep, _, _ = check_case("c3_bf16e", "bf16", logpsi_tol=BF16_LOGPSI_TOL, **BF16)
+    assert rep.clean_rows >= 0.8 * rep.rows
+
+
+def test_c4_bf16():
+    rep, _, _ = check_case("c4_bf16e", "bf16", logpsi_tol=BF16_LOGPSI_TOL_DEEP, **BF16)
+    assert rep.clean_rows >= 0.4 * rep.rows
+
+
+def test_c5_bf16():
+    rep, _, _ = check_case("c5_bf16e", "bf16", logpsi_tol=BF16_LOGPSI_TOL_C5, **BF16)
+    assert rep.clean_rows >= 0.1 * rep.rows
+
+
+# ---- micro-batch boundaries ----
+
+@pytest.mark.parametrize("case,precision,tol", [
+    ("c4_fp64", "fp32", {}),
+    ("c4_bf16e", "bf16", dict(logpsi_tol=BF16_LOGPSI_TOL_DEEP, **BF16)),
+    ("c3_bf16e", "bf16", dict(logpsi_tol=BF16_LOGPSI_TOL, **BF16)),
+])
+def test_multi_micro_batch(case, precision, tol):
+    """Three or more micro-batches: per-sample outputs bit-identical to the
+    single-micro-batch run, and parity against the reference holds across
+    the boundaries (the bench runs c4 as ~18 micro-batches)."""
+    _, e1, l1 = check_case(case, precision, 0, **tol)
+    n = load_fixture(os.path.join(GOLDEN, f"parity_{case}.npz"))[0]["samples"].shape[0]
+    mb = max(1, -(-n // 3))
+    _, e3, l3 = check_case(case, precision, mb, **tol)
+    assert np.array_equal(e1, e3) and np.array_equal(l1, l3)
+    engine(str(load_fixture(os.path.join(GOLDEN, f"parity_{case}.npz"))[0]["workload"]),
+           precision)[2].set_micro_batch(0)
