@@ -282,12 +282,14 @@ class LocalEnergyEngine:
         return lp[:K]
 
     def taps(self, batch):
-        """Per-sample K, U[L+1], per-location codes [L, K*T] and row log-probs."""
+        """Per-sample K, U[L+1], per-location codes [L, K*T, vq_heads] (-1 in
+        blocks without VQ) and row log-probs."""
         cfgs = np.ascontiguousarray(batch, np.uint8)
         B = cfgs.shape[0]
         L = self.cfg.n_layers
         T = self.cfg.seq_len
-        cap = B * (self.n_bonds + 1) * T * L
+        H = self.cfg.vq_heads
+        cap = B * (self.n_bonds + 1) * T * L * H
         K = np.zeros(B, np.int32)
         U = np.zeros((B, L + 1), np.int64)
         codes = np.zeros(cap, np.int32)
@@ -298,8 +300,8 @@ class LocalEnergyEngine:
                                        N.ptr(lp, C.c_double), lpcap))
         out, lps, pos, lpos = [], [], 0, 0
         for s in range(B):
-            n = L * int(K[s]) * T
-            out.append(codes[pos:pos + n].reshape(L, int(K[s]) * T))
+            n = L * int(K[s]) * T * H
+            out.append(codes[pos:pos + n].reshape(L, int(K[s]) * T, H))
             lps.append(lp[lpos:lpos + int(K[s])])
             pos += n
             lpos += int(K[s])

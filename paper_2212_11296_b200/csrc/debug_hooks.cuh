@@ -82,10 +82,10 @@ extern "C" int vqnqs_debug_vq(int64_t M, int d, const float* x, const float* cb3
     const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;
     if (LOCS == 64) {
       smem_optin(reinterpret_cast<const void*>(k_vq<64>), vsmem);
-      k_vq<64><<<sms * 4, 256, vsmem>>>(dM, d, x, cb32, Q, code);
+      k_vq<64><<<sms * 4, 256, vsmem>>>(dM, d, d, x, cb32, Q, code, 1);
     } else {
       smem_optin(reinterpret_cast<const void*>(k_vq<32>), vsmem);
-      k_vq<32><<<sms * 4, 256, vsmem>>>(dM, d, x, cb32, Q, code);
+      k_vq<32><<<sms * 4, 256, vsmem>>>(dM, d, d, x, cb32, Q, code, 1);
     }
   }
   cudaError_t e = cudaGetLastError();

@@ -71,6 +71,7 @@ struct DBuf {
 };
 
 struct DevBlock {
+  bool has_vq, has_ffn;  // full blocks carry both (VQ when vq_enabled); the half block neither
   float *ln1_g, *ln1_b, *bqkv, *bo, *ln2_g, *ln2_b, *b1, *b2, *cb32, *wn2;
   float* pwo;  // per-code continuation table [Q x d]: code_j Wo + bo
   float wmax, werr;
@@ -131,13 +132,16 @@ class EngineImpl {
   int dev = 0;
   int sms = 148;
   cudaStream_t own = nullptr;
-  int d, nh, dh, Q, L, V, T, g, N, lastV;
+  int d, nh, dh, Q, H, L, V, T, g, N, lastV;
+  int qbits = 1;            // bits per VQ code in the packed tuple key
+  bool tuple_pass = false;  // H codes exceed 32 bits: number tuples first
   bool use_tc_gemm = false;  // tcgen05 per-location GEMMs (bf16)
   bool use_tc_vq = false;    // tcgen05 certified-argmin VQ (bf16)
   bool use_tc_attn = false;  // tcgen05 gathered attention (bf16)
   unsigned long long* d_rescored = nullptr;
   std::vector<void*> allocs;
   float *tok_embed, *pos_embed, *lnf_g, *lnf_b, *head_b;
+  float* zeros_d = nullptr;  // [d] zeros
   void* head_w;
   std::vector<DevBlock> blk;
   // hamiltonian
@@ -158,7 +162,8 @@ class EngineImpl {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> lev;  // per-layer stage events, read once per chunk
   DBuf<double> diag_, lpV_, lp_rows_;
-  DBuf<unsigned long long> tkey_;
+  DBuf<unsigned long long> tkey_, ctup_;
+  DBuf<int32_t> ckey_;  // packed / numbered VQ code tuples (H > 1)
   DBuf<float> x_a, x_b, y_, att_, xn2_, rr2_;
   DBuf<bf16> att_hi_, att_lo_;
   DBuf<char> h_, qkv_, f1_;
@@ -214,11 +219,7 @@ class EngineImpl {
     if (n_params != int(spec.size()))
       throw ShapeError("parameter count " + std::to_string(n_params) + " != " +
                        std::to_string(spec.size()));
-    if (!c.vq_enabled || c.trailing_half_block)
-      throw CapabilityError("GPU path: every block must carry a VQ (no half block, vq on)");
-    if (c.vq_heads != 1) throw CapabilityError("GPU path: vq_heads must be 1");
     if (c.group_size > 4) throw CapabilityError("GPU path: group_size <= 4");
-    if (c.d_hidden % 16 != 0) throw CapabilityError("GPU path: d_hidden % 16 == 0");
     if (precision != VQNQS_PREC_FP32 && precision != VQNQS_PREC_BF16)
       throw ConfigError("precision must be fp32 or bf16");
     int ndev = 0;
@@ -231,7 +232,8 @@ class EngineImpl {
     nh = c.n_heads;
     dh = d / nh;
     Q = c.vq_codebook;
-    L = c.n_blocks;
+    H = std::max(1, c.vq_heads);
+    L = c.n_blocks + (c.trailing_half_block ? 1 : 0);
     g = c.group_size;
     V = 1 << g;
     N = c.n_sites;
@@ -239,7 +241,15 @@ class EngineImpl {
     lastV = (N % g == 0) ? V : 1 << (N % g);
     if (T > 1024 || dh > 256) throw CapabilityError("GPU path: T <= 1024, head dim <= 256");
     use_tc_gemm = tc_gemm_ok(prec, d, d) && tc_gemm_ok(prec, 4 * d, d);
-    use_tc_vq = tc_vq_ok(prec, d, Q);
+    use_tc_vq = H == 1 && c.vq_enabled && tc_vq_ok(prec, d, Q);
+    // dedup key of a location after a VQ: (residual row, code tuple); H codes
+    // of ceil(log2 Q) bits pack into the key's low 32 bits when they fit,
+    // otherwise the tuple is first numbered by its own exact-key pass
+    qbits = 1;
+    while ((int64_t(1) << qbits) < Q) ++qbits;
+    tuple_pass = H > 1 && H * qbits > 32;
+    if (H > 1 && H * qbits > 63)
+      throw CapabilityError("GPU path: vq_heads * ceil(log2 vq_codebook) <= 63");
     use_tc_attn = tc_attn_ok(prec, d, dh, T) && !getenv("VQNQS_SIMT_ATTENTION");
     ntiles_.ensure(1);
     CK(cudaMalloc(&d_rescored, sizeof(unsigned long long)));
@@ -252,12 +262,25 @@ class EngineImpl {
     pos_embed = upload_f(nxt(), numel(1));
     for (int b = 0; b < L; ++b) {
       DevBlock B{};
+      // the trailing half block is attention only (no FFN, no VQ);
+      // proj/src/model.cpp:113-184
+      B.has_ffn = b < c.n_blocks;
+      B.has_vq = B.has_ffn && c.vq_enabled;
       const double* ln1g = nxt();
       const double* ln1b = nxt();
       const double *wq = nxt(), *bq = nxt(), *wk = nxt(), *bk = nxt(), *wv = nxt(), *bv = nxt(),
-                   *wo = nxt(), *bo = nxt(), *cb = nxt();
-      const double *ln2g = nxt(), *ln2b = nxt(), *w1 = nxt(), *b1 = nxt(), *w2 = nxt(),
-                   *b2 = nxt();
+                   *wo = nxt(), *bo = nxt();
+      const double* cb = B.has_vq ? nxt() : nullptr;
+      const double *ln2g = nullptr, *ln2b = nullptr, *w1 = nullptr, *b1 = nullptr,
+                   *w2 = nullptr, *b2 = nullptr;
+      if (B.has_ffn) {
+        ln2g = nxt();
+        ln2b = nxt();
+        w1 = nxt();
+        b1 = nxt();
+        w2 = nxt();
+        b2 = nxt();
+      }
       B.ln1_g = upload_f(ln1g, d);
       B.ln1_b = upload_f(ln1b, d);
       std::vector<double> wqkv((size_t)d * 3 * d), bqkv(3 * d);
@@ -276,11 +299,12 @@ class EngineImpl {
       B.bqkv = upload_f(bqkv.data(), 3 * d);
       B.wo = upload_op(std::vector<double>(wo, wo + (size_t)d * d));
       B.bo = upload_f(bo, d);
-      B.cb32 = upload_f(cb, (int64_t)Q * d);
-      {
+      if (B.has_vq) {
+        // codebook [H*Q x d/H] (proj/src/model.cpp:139-142)
+        B.cb32 = upload_f(cb, (int64_t)Q * d);
         // bf16 operand copy, |W_j|^2, max |W_j| and the bf16 rounding error
         // of the codebook for the certified argmin (tc_vq.cuh)
-        const VqCodebook pc = prepare_codebook(cb, Q, d);
+        const VqCodebook pc = prepare_codebook(cb, H * Q, d / H);
         B.wn2 = upload(pc.wn2);
         B.wmax = float(pc.wmax);
         B.werr = float(pc.werr);
@@ -288,12 +312,14 @@ class EngineImpl {
         else B.cbA = upload_op(std::vector<double>(cb, cb + (size_t)Q * d));
         if (use_tc_vq) B.tmB = make_tmap_bf16(B.cbA, uint64_t(Q), uint64_t(d), 256);
       }
-      B.ln2_g = upload_f(ln2g, d);
-      B.ln2_b = upload_f(ln2b, d);
-      B.w1 = upload_op(std::vector<double>(w1, w1 + (size_t)d * 4 * d));
-      B.b1 = upload_f(b1, 4 * d);
-      B.w2 = upload_op(std::vector<double>(w2, w2 + (size_t)4 * d * d));
-      B.b2 = upload_f(b2, d);
+      if (B.has_ffn) {
+        B.ln2_g = upload_f(ln2g, d);
+        B.ln2_b = upload_f(ln2b, d);
+        B.w1 = upload_op(std::vector<double>(w1, w1 + (size_t)d * 4 * d));
+        B.b1 = upload_f(b1, 4 * d);
+        B.w2 = upload_op(std::vector<double>(w2, w2 + (size_t)4 * d * d));
+        B.b2 = upload_f(b2, d);
+      }
       if (use_tc_gemm) {
         auto tr = [](const double* w, int rows, int cols) {
           std::vector<double> t((size_t)rows * cols);
@@ -303,8 +329,10 @@ class EngineImpl {
         };
         B.wqkvT = upload_op(tr(wqkv.data(), d, 3 * d));
         B.woT = upload_op(tr(wo, d, d));
-        B.w1T = upload_op(tr(w1, d, 4 * d));
-        B.w2T = upload_op(tr(w2, 4 * d, d));
+        if (B.has_ffn) {
+          B.w1T = upload_op(tr(w1, d, 4 * d));
+          B.w2T = upload_op(tr(w2, 4 * d, d));
+        }
       }
       blk.push_back(B);
     }
@@ -316,7 +344,10 @@ class EngineImpl {
     // Per-code continuation tables: o_j = code_j Wo + bo for every codeword,
     // with the same GEMM (and so the same per-row arithmetic) the per-row
     // continuation would run — the values are bit-identical, and the Wo GEMM
-    // leaves the per-step path (hard part 7).
+    // leaves the per-step path (hard part 7). With H VQ heads the
+    // quantized row is H codewords side by side, so a Wo + bo =
+    // bo + sum_h code_{h,j_h} Wo[rows of head h]: one [Q x d] table per head
+    // (bo folded into head 0's), summed per row by k_cont_ln.
     {
       int64_t* dQ = nullptr;
       float* zeros = nullptr;
@@ -325,21 +356,34 @@ class EngineImpl {
       CK(cudaMemcpy(dQ, &q64, sizeof(int64_t), cudaMemcpyHostToDevice));
       CK(cudaMalloc(&zeros, size_t(Q) * d * sizeof(float)));
       CK(cudaMemset(zeros, 0, size_t(Q) * d * sizeof(float)));
+      const int hd = d / H;
       for (auto& B : blk) {
-        CK(cudaMalloc(&B.pwo, size_t(Q) * d * sizeof(float)));
+        if (!B.has_vq) continue;
+        CK(cudaMalloc(&B.pwo, size_t(H) * Q * d * sizeof(float)));
         allocs.push_back(B.pwo);
-        if (prec == VQNQS_PREC_BF16)
-          gemm<bf16>(dQ, Q, d, d, B.cbA, d, nullptr, B.wo, B.woT, B.bo, B.pwo, d, EPI_RESID, zeros,
-                     d, nullptr, own);
-        else
-          gemm<float>(dQ, Q, d, d, B.cbA, d, nullptr, B.wo, B.woT, B.bo, B.pwo, d, EPI_RESID,
-                      zeros, d, nullptr, own);
+        for (int h = 0; h < H; ++h) {
+          const size_t aoff = size_t(h) * Q * hd * esz(), boff = size_t(h) * hd * d * esz();
+          const void* A = static_cast<const char*>(B.cbA) + aoff;
+          const void* W = static_cast<const char*>(B.wo) + boff;
+          const void* WT = H == 1 ? B.woT : nullptr;  // tcgen05 needs the full K = d
+          float* out = B.pwo + size_t(h) * Q * d;
+          const float* bias = h == 0 ? B.bo : zeros;
+          if (prec == VQNQS_PREC_BF16)
+            gemm<bf16>(dQ, Q, d, hd, A, hd, nullptr, W, WT, bias, out, d, EPI_RESID, zeros, d,
+                       nullptr, own);
+          else
+            gemm<float>(dQ, Q, d, hd, A, hd, nullptr, W, WT, bias, out, d, EPI_RESID, zeros, d,
+                        nullptr, own);
+        }
       }
       CK(cudaStreamSynchronize(own));
       CK(cudaGetLastError());
       cudaFree(dQ);
       cudaFree(zeros);
     }
+    CK(cudaMalloc(&zeros_d, size_t(d) * sizeof(float)));
+    allocs.push_back(zeros_d);
+    CK(cudaMemset(zeros_d, 0, size_t(d) * sizeof(float)));
   }
 
   ~EngineImpl() {
@@ -362,7 +406,7 @@ class EngineImpl {
     slot_.release(); rep_of_.release(); trep_.release(); tuid_.release(); g_code_.release();
     lpos_.release(); upos_.release(); row_aoff_.release(); act_off_.release(); tab_off_.release();
     Uoff_.release(); tot_.release(); g_res_.release(); attw_.release(); diag_.release(); lpV_.release();
-    lp_rows_.release(); tkey_.release(); x_a.release(); x_b.release(); y_.release();
+    lp_rows_.release(); tkey_.release(); ctup_.release(); ckey_.release(); x_a.release(); x_b.release(); y_.release();
     att_.release(); xn2_.release(); rr2_.release(); att_hi_.release(); att_lo_.release(); h_.release(); qkv_.release(); f1_.release(); cfg_stage_.release();
     out_stage_.release(); taps_codes_.release();
   }
@@ -440,6 +484,29 @@ class EngineImpl {
     ++launches;
   }
 
+  // CUDA-core nearest codeword per location and VQ head (k_vq once per
+  // head): codes [M x H]
+  void vq_simt(const int64_t* Mp, int64_t Mcap, const float* att, const float* cb32,
+               int32_t* code, cudaStream_t st) {
+    const int hd = d / H;
+    const int LOCS = hd > 384 ? 32 : 64;
+    const size_t vsmem = (size_t(LOCS) * (hd + 1) + 32 * size_t(hd + 1) + 2 * 256) * 4;
+    const int vgrid =
+        int(std::max<int64_t>(1, std::min<int64_t>((Mcap + LOCS - 1) / LOCS, sms * 4)));
+    for (int h = 0; h < H; ++h) {
+      const float* x = att + size_t(h) * hd;
+      const float* cb = cb32 + size_t(h) * Q * hd;
+      if (LOCS == 64) {
+        smem_optin(reinterpret_cast<const void*>(k_vq<64>), vsmem);
+        k_vq<64><<<vgrid, 256, vsmem, st>>>(Mp, hd, d, x, cb, Q, code + h, H);
+      } else {
+        smem_optin(reinterpret_cast<const void*>(k_vq<32>), vsmem);
+        k_vq<32><<<vgrid, 256, vsmem, st>>>(Mp, hd, d, x, cb, Q, code + h, H);
+      }
+      ++launches;
+    }
+  }
+
   template <typename TA>
   void run_chunk(const uint8_t* d_cfg, int S, double* d_e, double* d_logpsi, cudaStream_t st,
                  std::vector<int32_t>& hK, std::vector<int32_t>& hU, Engine::Taps* taps,
@@ -466,8 +533,8 @@ class EngineImpl {
     CK(cudaStreamSynchronize(st));
     const int64_t M = totals[0], TB = totals[1];
     // arena
-    lrow_.ensure(M); lpos_.ensure(M); I_a.ensure(M); I_b.ensure(M); code_.ensure(M);
-    slot_.ensure(M); rep_of_.ensure(M); g_code_.ensure(M); g_res_.ensure(M); upos_.ensure(M);
+    lrow_.ensure(M); lpos_.ensure(M); I_a.ensure(M); I_b.ensure(M); code_.ensure(M * H);
+    slot_.ensure(M); rep_of_.ensure(M); g_code_.ensure(M * H); g_res_.ensure(M); upos_.ensure(M);
     if (tkey_.n < size_t(TB)) {
       tkey_.ensure(TB); trep_.ensure(TB); tuid_.ensure(TB);
       CK(cudaMemsetAsync(tkey_.p, 0xFF, tkey_.n * sizeof(unsigned long long), st));
@@ -475,8 +542,10 @@ class EngineImpl {
     }
     x_a.ensure(M * d); x_b.ensure(M * d); y_.ensure(M * d);
     h_.ensure(M * d * esz()); qkv_.ensure(M * 3 * d * esz()); f1_.ensure(M * 4 * d * esz());
-    if (!use_tc_attn) att_.ensure(M * d);  // fp32 attention rows (CUDA-core path)
-    if (use_tc_vq) {
+    // fp32 attention rows: the CUDA-core attention's output, or the
+    // CUDA-core quantizer's input
+    if (!use_tc_attn || !use_tc_vq) att_.ensure(M * d);
+    if (use_tc_vq || use_tc_attn) {
       att_hi_.ensure(M * d);
       att_lo_.ensure(M * d);
       xn2_.ensure(M);
@@ -491,13 +560,15 @@ class EngineImpl {
     int32_t* Inext = I_b.p;
     k_dedup<0><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
                                   slot_.p, lrow_.p, lpos_.p, tok0_.p, row_bond_.p, d_bonds, R1, T,
-                                  g, V, nullptr, nullptr, int(dense), Icur, rep_of_.p, Ucnt_.p);
+                                  g, V, nullptr, nullptr, int(dense), Icur, rep_of_.p, Ucnt_.p,
+                                  nullptr);
     k_scan<<<1, 1024, 0, st>>>(S, Ucnt_.p, Uoff_.p, tot + 2, 0);
     k_embed<<<S, 256, 0, st>>>(d, R1, T, g, V, Ucnt_.p, Uoff_.p, act_off_.p, rep_of_.p, lrow_.p,
                                lpos_.p, tok0_.p, row_bond_.p, d_bonds, tok_embed, pos_embed, x_a.p);
     launches += 4;
     float* xcur = x_a.p;
     float* xnext = x_b.p;
+    float* ybuf = y_.p;
     const int lnGrid = sms * 8;
     const float scale = float(1.0 / std::sqrt(double(dh)));
     for (int b = 0; b < L; ++b) {
@@ -551,57 +622,110 @@ class EngineImpl {
             att_.p);
       }
       CK(cudaEventRecord(lev[3 * b + 2], st));
-      {
+      const int64_t* Mn = tot + 3 + b;
+      if (B.has_vq) {
         if (use_tc_vq) {
           if (!use_tc_attn) {
             k_vq_prep<<<sms * 8, 256, 0, st>>>(tot + 0, d, att_.p, att_hi_.p, att_lo_.p, xn2_.p,
                                                rr2_.p);
             ++launches;
           }
-          tc_vq(tot + 0, M, d, att_hi_.p, att_lo_.p, xn2_.p, rr2_.p, B.tmB, B.cb32, B.wn2, B.wmax, B.werr, Q,
-                code_.p, d_rescored, vqs_, st, sms);
-          ++launches;
+          tc_vq(tot + 0, M, d, att_hi_.p, att_lo_.p, xn2_.p, rr2_.p, B.tmB, B.cb32, B.wn2, B.wmax,
+                B.werr, Q, code_.p, d_rescored, vqs_, st, sms);
+          launches += 2;
         } else {
-          const int LOCS = d > 384 ? 32 : 64;
-          const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;
-          const int vgrid =
-              int(std::max<int64_t>(1, std::min<int64_t>((M + LOCS - 1) / LOCS, sms * 4)));
-          if (LOCS == 64) {
-            smem_optin(reinterpret_cast<const void*>(k_vq<64>), vsmem);
-            k_vq<64><<<vgrid, 256, vsmem, st>>>(tot + 0, d, att_.p, B.cb32, Q, code_.p);
+          if (use_tc_attn) {  // x = xh + xl for the CUDA-core quantizer
+            k_join_split<<<sms * 8, 256, 0, st>>>(tot + 0, d, att_hi_.p, att_lo_.p, att_.p);
+            ++launches;
+          }
+          vq_simt(tot + 0, M, att_.p, B.cb32, code_.p, st);
+        }
+        CK(cudaEventRecord(lev[3 * b + 1], st));
+        if (tap_codes) {
+          std::vector<int32_t> hc(size_t(M) * H);
+          CK(cudaMemcpyAsync(hc.data(), code_.p, hc.size() * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          tap_codes->insert(tap_codes->end(), hc.begin(), hc.end());
+        }
+        // requantize (proj/src/dedup.cpp:136-185): key (residual row, codes)
+        const int32_t* ckey = code_.p;
+        if (H > 1) {
+          ckey_.ensure(M);
+          if (tuple_pass) {
+            ctup_.ensure(M);
+            k_pack_codes<<<int((M + 255) / 256), 256, 0, st>>>(tot + 0, H, qbits, code_.p,
+                                                               ctup_.p, nullptr);
+            k_dedup<2><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p,
+                                          tuid_.p, slot_.p, nullptr, nullptr, nullptr, nullptr,
+                                          nullptr, R1, T, g, V, nullptr, nullptr, int(dense),
+                                          ckey_.p, rep_of_.p, Uc_next, ctup_.p);
+            launches += 2;
           } else {
-            smem_optin(reinterpret_cast<const void*>(k_vq<32>), vsmem);
-            k_vq<32><<<vgrid, 256, vsmem, st>>>(tot + 0, d, att_.p, B.cb32, Q, code_.p);
+            k_pack_codes<<<int((M + 255) / 256), 256, 0, st>>>(tot + 0, H, qbits, code_.p,
+                                                               nullptr, ckey_.p);
+            ++launches;
+          }
+          ckey = ckey_.p;
+        }
+        k_dedup<1><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
+                                      slot_.p, nullptr, nullptr, nullptr, nullptr, nullptr, R1, T,
+                                      g, V, Icur, ckey, int(dense), Inext, rep_of_.p, Uc_next,
+                                      nullptr);
+        k_scan<<<1, 1024, 0, st>>>(S, Uc_next, Uo_next, tot + 3 + b, 0);
+        k_build_gather<<<S, 256, 0, st>>>(H, Uc_next, Uo_next, Uo_cur, act_off_.p, rep_of_.p,
+                                          code_.p, Icur, lpos_.p, g_code_.p, g_res_.p, upos_.p);
+        launches += 3;
+        // continuation (proj/src/dedup.cpp:246-267): y = r + (code rows Wo + bo)
+        // from the per-code tables, fused with LN2
+        k_cont_ln<TA><<<lnGrid, 256, 0, st>>>(Mn, d, H, Q, xcur, g_res_.p, g_code_.p, B.pwo,
+                                              B.ln2_g, B.ln2_b, ybuf, h);
+        ++launches;
+        gemm<TA>(Mn, M, 4 * d, d, h, d, nullptr, B.w1, B.w1T, B.b1, f1, 4 * d, EPI_GELU, nullptr,
+                 0, nullptr, st);
+        gemm<TA>(Mn, M, d, 4 * d, f1, 4 * d, nullptr, B.w2, B.w2T, B.b2, xnext, d, EPI_RESID,
+                 ybuf, d, nullptr, st);
+        std::swap(xcur, xnext);
+      } else {
+        // a block without VQ: densify_attention (proj/src/dedup.cpp:187-211),
+        // every location its own row (the reference's U = K T; here the
+        // active locations, the others being the base row's), then
+        // y = r + (att Wo + bo) and, in a full block, the FFN
+        CK(cudaEventRecord(lev[3 * b + 1], st));
+        if (tap_codes) tap_codes->insert(tap_codes->end(), size_t(M) * H, -1);
+        k_densify<<<S, 256, 0, st>>>(Mact_.p, act_off_.p, Uo_cur, Icur, lpos_.p, Inext, g_res_.p,
+                                     upos_.p, Uc_next);
+        k_scan<<<1, 1024, 0, st>>>(S, Uc_next, Uo_next, tot + 3 + b, 0);
+        k_gather_rows<<<lnGrid, 256, 0, st>>>(Mn, d, xcur, g_res_.p, ybuf);
+        launches += 3;
+        const void* A = att_.p;  // fp32 engine: the fp32 attention rows
+        if (prec == VQNQS_PREC_BF16) {
+          if (use_tc_attn) {
+            A = att_hi_.p;  // bf16(x): the operand the emulated reference rounds to
+          } else {
+            k_to_bf16<<<lnGrid, 256, 0, st>>>(tot + 0, d, att_.p,
+                                              reinterpret_cast<bf16*>(h));
+            ++launches;
+            A = h;
           }
         }
-        launches += 2;
+        gemm<TA>(Mn, M, d, d, A, d, nullptr, B.wo, B.woT, B.bo, xnext, d, EPI_RESID, ybuf, d,
+                 nullptr, st);
+        if (B.has_ffn) {
+          k_layernorm<TA><<<lnGrid, 256, 0, st>>>(Mn, d, xnext, B.ln2_g, B.ln2_b, h);
+          ++launches;
+          gemm<TA>(Mn, M, 4 * d, d, h, d, nullptr, B.w1, B.w1T, B.b1, f1, 4 * d, EPI_GELU,
+                   nullptr, 0, nullptr, st);
+          gemm<TA>(Mn, M, d, 4 * d, f1, 4 * d, nullptr, B.w2, B.w2T, B.b2, ybuf, d, EPI_RESID,
+                   xnext, d, nullptr, st);
+          float* old = xcur;  // the block output is in ybuf
+          xcur = ybuf;
+          ybuf = xnext;
+          xnext = old;
+        } else {
+          std::swap(xcur, xnext);
+        }
       }
-      CK(cudaEventRecord(lev[3 * b + 1], st));
-      if (tap_codes) {
-        taps_codes_.ensure(M);
-        std::vector<int32_t> hc(M);
-        CK(cudaMemcpyAsync(hc.data(), code_.p, M * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        tap_codes->insert(tap_codes->end(), hc.begin(), hc.end());
-      }
-      k_dedup<1><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
-                                    slot_.p, nullptr, nullptr, nullptr, nullptr, nullptr, R1, T, g,
-                                    V, Icur, code_.p, int(dense), Inext, rep_of_.p, Uc_next);
-      k_scan<<<1, 1024, 0, st>>>(S, Uc_next, Uo_next, tot + 3 + b, 0);
-      k_build_gather<<<S, 256, 0, st>>>(Uc_next, Uo_next, Uo_cur, act_off_.p, rep_of_.p, code_.p,
-                                        Icur, lpos_.p, g_code_.p, g_res_.p, upos_.p);
-      launches += 3;
-      const int64_t* Mn = tot + 3 + b;
-      // continuation (proj/src/dedup.cpp:246-267): y = r + (code_row Wo + bo)
-      // from the per-code table, fused with LN2
-      k_cont_ln<TA><<<lnGrid, 256, 0, st>>>(Mn, d, xcur, g_res_.p, g_code_.p, B.pwo, B.ln2_g,
-                                            B.ln2_b, y_.p, h);
-      ++launches;
-      gemm<TA>(Mn, M, 4 * d, d, h, d, nullptr, B.w1, B.w1T, B.b1, f1, 4 * d, EPI_GELU, nullptr, 0,
-               nullptr, st);
-      gemm<TA>(Mn, M, d, 4 * d, f1, 4 * d, nullptr, B.w2, B.w2T, B.b2, xnext, d, EPI_RESID, y_.p, d,
-               nullptr, st);
-      std::swap(xcur, xnext);
       std::swap(Icur, Inext);
     }
     // (e) head and E_loc
@@ -654,9 +778,11 @@ class EngineImpl {
     // algorithmic work of the attention->VQ stage actually executed
     double aw = 0;
     for (int s2 = 0; s2 < S; ++s2) aw += double(haw[s2]);
-    prof[1] += double(L) * (4.0 * d * aw + 2.0 * double(d) * Q * double(M));
+    int nvq = 0;
+    for (const auto& Bk : blk) nvq += Bk.has_vq ? 1 : 0;
+    prof[1] += double(L) * 4.0 * d * aw + double(nvq) * 2.0 * double(d) * Q * double(M);
     prof[9] += double(L) * 4.0 * d * aw;            // attention (QK^T + PV, live keys)
-    prof[10] += double(L) * 2.0 * double(d) * Q * double(M);  // VQ distance GEMM
+    prof[10] += double(nvq) * 2.0 * double(d) * Q * double(M);  // VQ distance GEMM
     prof[3] += double(M) * L;
     prof[11] += double(h_ntiles) * L;  // attention tiles (<= 128 locations each)
     for (int s2 = 0; s2 < S; ++s2)
@@ -698,6 +824,11 @@ class EngineImpl {
       for (int s = 0; s < S; ++s) {
         std::vector<int64_t> U(L + 1);
         for (int b = 0; b <= L; ++b) U[b] = hU[size_t(b) * S + s];
+        // a block without VQ densifies: the reference counts every one of
+        // the K T locations as a unique row (the engine computes the active
+        // ones; the rest are the base row's, identical by causality)
+        for (int b = 0; b < L; ++b)
+          if (!blk[b].has_vq) U[b + 1] = int64_t(hK[s]) * T;
         if (ledger7) ledger_add(c, hK[s], U.data(), ledger7);
         if (taps) {
           if (taps->K) taps->K[s0 + s] = hK[s];
@@ -707,11 +838,11 @@ class EngineImpl {
       }
       if (taps) {
         const int R1 = nb + 1;
-        const int64_t M = int64_t(tcodes.size()) / std::max(1, L);
+        const int64_t M = int64_t(tcodes.size()) / std::max(1, L * H);
         for (int s = 0; s < S; ++s) {
           const int Ks = hK[s];
           if (taps->codes) {
-            if (tap_code_pos + int64_t(L) * Ks * T > taps->codes_cap)
+            if (tap_code_pos + int64_t(L) * Ks * T * H > taps->codes_cap)
               throw ShapeError("taps: codes buffer too small");
             for (int b = 0; b < L; ++b)
               for (int k = 0; k < Ks; ++k) {
@@ -719,11 +850,12 @@ class EngineImpl {
                 const int a = k == 0 ? 0 : tt1[r] + 1;
                 for (int p = 0; p < T; ++p) {
                   const int64_t loc = p < a ? tact[s] + p : tact[s] + taoff[r] + (p - a);
-                  taps->codes[tap_code_pos + (int64_t(b) * Ks + k) * T + p] =
-                      tcodes[size_t(b) * M + loc];
+                  for (int hh = 0; hh < H; ++hh)
+                    taps->codes[tap_code_pos + ((int64_t(b) * Ks + k) * T + p) * H + hh] =
+                        tcodes[(size_t(b) * M + loc) * H + hh];
                 }
               }
-            tap_code_pos += int64_t(L) * Ks * T;
+            tap_code_pos += int64_t(L) * Ks * T * H;
           }
           if (taps->lp_rows) {
             if (tap_lp_pos + Ks > taps->lp_cap) throw ShapeError("taps: lp buffer too small");
@@ -759,7 +891,7 @@ class EngineImpl {
     f1.ensure(size_t(B) * 4 * d * es);
     kc.ensure(size_t(L) * B * T * d * es);
     vc.ensure(size_t(L) * B * T * d * es);
-    code.ensure(B);
+    code.ensure(size_t(B) * H);
     dB.ensure(1);
     iota.ensure(B);
     pos.ensure(B);
@@ -799,27 +931,39 @@ class EngineImpl {
         k_dec_attention<TA><<<int((jobs + awpb - 1) / awpb), 32 * awpb, asmem, st>>>(
             B, d, nh, T, t, scale, qp, kcb, vcb, att.p);
         launches += 2;
+        if (!Bk.has_vq) {
+          // no VQ (model.cpp:325-355 with has_vq = false): x += att Wo + bo,
+          // then the FFN in a full block
+          const void* A = att.p;
+          if (prec == VQNQS_PREC_BF16) {
+            k_to_bf16<<<lnGrid, 256, 0, st>>>(dB.p, d, att.p, reinterpret_cast<bf16*>(hp));
+            ++launches;
+            A = hp;
+          }
+          gemm<TA>(dB.p, B, d, d, A, d, nullptr, Bk.wo, Bk.woT, Bk.bo, xn, d, EPI_RESID, xc, d,
+                   nullptr, st);
+          if (Bk.has_ffn) {
+            k_layernorm<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, xn, Bk.ln2_g, Bk.ln2_b, hp);
+            ++launches;
+            gemm<TA>(dB.p, B, 4 * d, d, hp, d, nullptr, Bk.w1, Bk.w1T, Bk.b1, fp, 4 * d,
+                     EPI_GELU, nullptr, 0, nullptr, st);
+            gemm<TA>(dB.p, B, d, 4 * d, fp, 4 * d, nullptr, Bk.w2, Bk.w2T, Bk.b2, xc, d,
+                     EPI_RESID, xn, d, nullptr, st);
+          } else {
+            std::swap(xc, xn);
+          }
+          continue;
+        }
         if (use_tc_vq) {
           k_vq_prep<<<sms * 8, 256, 0, st>>>(dB.p, d, att.p, xh.p, xl.p, xn2.p, rr2.p);
           tc_vq(dB.p, B, d, xh.p, xl.p, xn2.p, rr2.p, Bk.tmB, Bk.cb32, Bk.wn2, Bk.wmax, Bk.werr, Q,
                 code.p, nullptr, vqs_, st, sms);
           launches += 3;
         } else {
-          const int LOCS = d > 384 ? 32 : 64;
-          const size_t vsmem = (size_t(LOCS) * (d + 1) + 32 * size_t(d + 1) + 2 * 256) * 4;
-          const int vgrid = int(std::max<int64_t>(1, std::min<int64_t>((B + LOCS - 1) / LOCS,
-                                                                        int64_t(sms) * 4)));
-          if (LOCS == 64) {
-            smem_optin(reinterpret_cast<const void*>(k_vq<64>), vsmem);
-            k_vq<64><<<vgrid, 256, vsmem, st>>>(dB.p, d, att.p, Bk.cb32, Q, code.p);
-          } else {
-            smem_optin(reinterpret_cast<const void*>(k_vq<32>), vsmem);
-            k_vq<32><<<vgrid, 256, vsmem, st>>>(dB.p, d, att.p, Bk.cb32, Q, code.p);
-          }
-          ++launches;
+          vq_simt(dB.p, B, att.p, Bk.cb32, code.p, st);
         }
-        // continuation (proj/src/dedup.cpp:246-267) from the per-code Wo table
-        k_cont_ln<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, xc, iota.p, code.p, Bk.pwo, Bk.ln2_g,
+        // continuation (proj/src/dedup.cpp:246-267) from the per-code Wo tables
+        k_cont_ln<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, H, Q, xc, iota.p, code.p, Bk.pwo, Bk.ln2_g,
                                               Bk.ln2_b, y_.p, hp);
         ++launches;
         gemm<TA>(dB.p, B, 4 * d, d, hp, d, nullptr, Bk.w1, Bk.w1T, Bk.b1, fp, 4 * d, EPI_GELU,

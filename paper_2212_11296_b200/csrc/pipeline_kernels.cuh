@@ -293,6 +293,9 @@ __global__ void k_enumerate(int S, int R1, int T, const int32_t* __restrict__ K,
 // (compress_inputs, proj/src/dedup.cpp:52-76; requantize, :151-175).
 //   MODE 0 (input layer): key = (p, BOS-shifted token)      dedup.cpp:61-63
 //   MODE 1 (after VQ):    key = (residual row, VQ code)     dedup.cpp:156-159
+//                         (H > 1: the code tuple packed or numbered, k_pack_codes)
+//   MODE 2 (H > 1, wide tuples): key = the packed code tuple itself; the ids
+//                         number the distinct tuples of the sample for MODE 1
 // One CTA per sample; open-addressing table in global memory (L2-resident),
 // atomicCAS claims a slot, atomicMin keeps the first location, a block scan
 // over locations in order assigns ids. Slots are reset before exit so the
@@ -311,7 +314,9 @@ __global__ void __launch_bounds__(512) k_dedup(
     // no-reuse regime: every location is its own unique row
     int dense,
     // outputs
-    int32_t* __restrict__ I_out, int32_t* __restrict__ rep_of, int32_t* __restrict__ Ucnt) {
+    int32_t* __restrict__ I_out, int32_t* __restrict__ rep_of, int32_t* __restrict__ Ucnt,
+    // MODE 2 input
+    const unsigned long long* __restrict__ tup) {
   __shared__ int wtot[32];
   __shared__ int run_s;
   const int s = blockIdx.x;
@@ -333,8 +338,10 @@ __global__ void __launch_bounds__(512) k_dedup(
       const int sidx = r / R1;
       const int tok = p == 0 ? V : row_token(tok0 + (int64_t)sidx * T, bonds, row_bond[r], g, p - 1);
       key = (unsigned long long)p * (unsigned long long)(V + 1) + (unsigned long long)tok;
-    } else {
+    } else if (MODE == 1) {
       key = ((unsigned long long)(uint32_t)I_in[loc] << 32) | (uint32_t)code[loc];
+    } else {
+      key = tup[loc];
     }
     int64_t h = (int64_t)(hash64(key) & (uint64_t)(cap - 1));
     for (;;) {
@@ -486,7 +493,8 @@ __global__ void k_layernorm(const int64_t* __restrict__ Mp, int d, const float* 
 // so each row's o is bit-identical to a per-row product), then LN2(y).
 // One warp per row; y is kept for the W2 residual.
 template <typename TA>
-__global__ void k_cont_ln(const int64_t* __restrict__ Mp, int d, const float* __restrict__ x,
+__global__ void k_cont_ln(const int64_t* __restrict__ Mp, int d, int H, int Q,
+                          const float* __restrict__ x,
                           const int64_t* __restrict__ g_res, const int32_t* __restrict__ g_code,
                           const float* __restrict__ pwo, const float* __restrict__ gam,
                           const float* __restrict__ bet, float* __restrict__ y,
@@ -496,8 +504,31 @@ __global__ void k_cont_ln(const int64_t* __restrict__ Mp, int d, const float* __
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
     const float* xr = x + g_res[r] * d;
-    const float* pr = pwo + (int64_t)g_code[r] * d;
+    const float* pr = pwo + (int64_t)g_code[r * H] * d;
     float* yr = y + r * d;
+    if (H > 1) {
+      // H VQ heads: o = sum_h table_h[code_h] (head 0's table carries bo)
+      double s = 0.0;
+      for (int c = lane; c < d; c += 32) {
+        float o = pr[c];
+        for (int hh = 1; hh < H; ++hh)
+          o += pwo[((int64_t)hh * Q + g_code[r * H + hh]) * d + c];
+        const float v = xr[c] + o;
+        yr[c] = v;
+        s += v;
+      }
+      const double mean = warp_sum(s) / d;
+      double q = 0.0;
+      for (int c = lane; c < d; c += 32) {
+        const double t = yr[c] - mean;
+        q += t * t;
+      }
+      const double var = warp_sum(q) / d;
+      const double rstd = 1.0 / sqrt(var + 1e-5);
+      for (int c = lane; c < d; c += 32)
+        out[r * d + c] = from_f<TA>((float)((yr[c] - mean) * rstd * gam[c] + bet[c]));
+      continue;
+    }
     if (d <= 32 * LN_REG) {
       // y kept in registers between the passes; same sums
       float yv[LN_REG];
@@ -551,7 +582,7 @@ __global__ void k_cont_ln(const int64_t* __restrict__ Mp, int d, const float* __
 // For each new unique row (global id g): which codebook row and which
 // residual row it concatenates (requantize's V' = [code row || residual row],
 // proj/src/dedup.cpp:176-184), and its token position.
-__global__ void k_build_gather(const int32_t* __restrict__ Ucnt_next,
+__global__ void k_build_gather(int H, const int32_t* __restrict__ Ucnt_next,
                                const int64_t* __restrict__ Uoff_next,
                                const int64_t* __restrict__ Uoff_cur,
                                const int64_t* __restrict__ act_off,
@@ -565,10 +596,79 @@ __global__ void k_build_gather(const int32_t* __restrict__ Ucnt_next,
   for (int uid = threadIdx.x; uid < U; uid += blockDim.x) {
     const int64_t loc = base + rep_of[base + uid];
     const int64_t gi = Uoff_next[s] + uid;
-    g_code[gi] = code[loc];
+    for (int h = 0; h < H; ++h) g_code[gi * H + h] = code[loc * H + h];
     g_res[gi] = Uoff_cur[s] + I_cur[loc];
     upos[gi] = lpos[loc];
   }
+}
+
+// Blocks without a VQ (the trailing half block; every block when VQ is
+// off): densify_attention (proj/src/dedup.cpp:187-211) makes every location
+// its own unique row, with the residual row it concatenates. Over the
+// active locations that is the identity; the new rows' global ids equal the
+// location index (Uoff_next = act_off). One CTA per sample.
+__global__ void k_densify(const int32_t* __restrict__ Mact, const int64_t* __restrict__ act_off,
+                          const int64_t* __restrict__ Uoff_cur, const int32_t* __restrict__ I_cur,
+                          const int16_t* __restrict__ lpos, int32_t* __restrict__ I_next,
+                          int64_t* __restrict__ g_res, int16_t* __restrict__ upos,
+                          int32_t* __restrict__ Ucnt_next) {
+  const int s = blockIdx.x;
+  const int M = Mact[s];
+  const int64_t base = act_off[s];
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    I_next[base + i] = i;
+    g_res[base + i] = Uoff_cur[s] + I_cur[base + i];
+    upos[base + i] = lpos[base + i];
+  }
+  if (threadIdx.x == 0) Ucnt_next[s] = M;
+}
+
+// out[r] = x[g[r]] for r < *Mp rows of d floats (the residual rows of a
+// densified block, contiguous for the Wo GEMM's residual epilogue).
+__global__ void k_gather_rows(const int64_t* __restrict__ Mp, int d, const float* __restrict__ x,
+                              const int64_t* __restrict__ g, float* __restrict__ out) {
+  const int64_t M = *Mp;
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
+    const float* src = x + g[r] * d;
+    for (int c = lane; c < d; c += 32) out[r * d + c] = src[c];
+  }
+}
+
+// bf16 copy of *Mp fp32 rows of d (a bf16 engine's Wo operand when the
+// attention ran on CUDA cores).
+__global__ void k_to_bf16(const int64_t* __restrict__ Mp, int d, const float* __restrict__ x,
+                          bf16* __restrict__ out) {
+  const int64_t n = *Mp * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(x[i]);
+}
+
+// x = xh + xl (the tcgen05 attention's two-term split) as fp32 rows, for the
+// CUDA-core quantizer (vq_heads > 1).
+__global__ void k_join_split(const int64_t* __restrict__ Mp, int d, const bf16* __restrict__ xh,
+                             const bf16* __restrict__ xl, float* __restrict__ out) {
+  const int64_t n = *Mp * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __bfloat162float(xh[i]) + __bfloat162float(xl[i]);
+}
+
+// The H codes of a location as one exact key: code_h << (h * qbits), either
+// as 32 bits (key32, the MODE 1 code operand directly) or 64 bits (tup, to be
+// numbered by k_dedup<2> first).
+__global__ void k_pack_codes(const int64_t* __restrict__ Mp, int H, int qbits,
+                             const int32_t* __restrict__ code, unsigned long long* __restrict__ tup,
+                             int32_t* __restrict__ key32) {
+  const int64_t M = *Mp;
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (l >= M) return;
+  unsigned long long k = 0;
+  for (int h = 0; h < H; ++h) k |= (unsigned long long)(uint32_t)code[l * H + h] << (h * qbits);
+  if (tup) tup[l] = k;
+  if (key32) key32[l] = (int32_t)(uint32_t)k;
 }
 
 // ---------------------------------------------------------------- (e)

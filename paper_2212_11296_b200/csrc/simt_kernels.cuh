@@ -43,13 +43,14 @@ __global__ void __launch_bounds__(256) k_gemm_simt(
         const int r = e >> 4, kk = e & 15;
         const int64_t m = m0 + r;
         float v = 0.f;
-        if (m < M) {
+        if (m < M && k0 + kk < K) {
           const int64_t ar = gA ? (int64_t)gA[m] : m;
           v = to_f<TA>(A[ar * lda + k0 + kk]);
         }
         As[kk][r] = v;
         const int kb = e >> 6, n = e & 63;
-        Bs[kb][n] = (n0 + n < N) ? to_f<TA>(B[(int64_t)(k0 + kb) * N + n0 + n]) : 0.f;
+        Bs[kb][n] =
+            (n0 + n < N && k0 + kb < K) ? to_f<TA>(B[(int64_t)(k0 + kb) * N + n0 + n]) : 0.f;
       }
       __syncthreads();
 #pragma unroll
@@ -157,14 +158,17 @@ __global__ void __launch_bounds__(128) k_attention(
   }
 }
 
-// Nearest codeword per location (vq_apply_rows, proj/src/model.cpp:283-319,
-// H = 1): argmin_j sum_c (x_c - W_jc)^2 in fp32, ties to the lowest j.
-// LOCS locations per CTA x 32-code chunks staged in shared memory.
+// Nearest codeword per location and VQ head (vq_apply_rows,
+// proj/src/model.cpp:283-319): argmin_j sum_c (x_c - W_jc)^2 in fp32 over one
+// head's d columns (row stride ldx), ties to the lowest j; the pick goes to
+// code[l * cstride]. With H heads the engine launches once per head with x,
+// cb and code offset to that head. LOCS locations per CTA x 32-code chunks
+// staged in shared memory.
 template <int LOCS>
-__global__ void __launch_bounds__(256) k_vq(const int64_t* __restrict__ Mp, int d,
+__global__ void __launch_bounds__(256) k_vq(const int64_t* __restrict__ Mp, int d, int ldx,
                                             const float* __restrict__ att,
                                             const float* __restrict__ cb, int Q,
-                                            int32_t* __restrict__ code) {
+                                            int32_t* __restrict__ code, int cstride) {
   extern __shared__ float sm[];
   constexpr int G = 256 / LOCS;  // code groups per chunk
   constexpr int CH = 32;         // codes per chunk
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(256) k_vq(const int64_t* __restrict__ Mp, int 
   for (int64_t l0 = (int64_t)blockIdx.x * LOCS; l0 < M; l0 += (int64_t)gridDim.x * LOCS) {
     for (int idx = tid; idx < LOCS * d; idx += 256) {
       const int r = idx / d, c = idx % d;
-      X[r * (d + 1) + c] = (l0 + r < M) ? att[(l0 + r) * d + c] : 0.f;
+      X[r * (d + 1) + c] = (l0 + r < M) ? att[(l0 + r) * ldx + c] : 0.f;
     }
     float best = INFINITY;
     int bj = 0;
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(256) k_vq(const int64_t* __restrict__ Mp, int 
           j = vj;
         }
       }
-      code[l0 + li] = j;
+      code[(l0 + li) * cstride] = j;
     }
     __syncthreads();
   }

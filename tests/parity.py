@@ -154,19 +154,20 @@ def load_fixture(path):
 
 def compare(rep: ParityReport, taps, ref_e, ref_lpsi, gpu_codes, gpu_U, gpu_e, gpu_lpsi,
             gpu_lp_rows, T, coeffs=None):
-    """One sample. taps: oracle Taps (codes [L, K*T, 1], gaps [L, K*T], lp [K],
-    U [L+1]); gpu_codes [L, K*T]; gpu_U [L+1]; gpu_lp_rows [K]; coeffs: the
+    """One sample. taps: oracle Taps (codes [L, K*T, H], gaps [L, K*T], lp [K],
+    U [L+1]); gpu_codes [L, K*T, H]; gpu_U [L+1]; gpu_lp_rows [K]; coeffs: the
     sample's connected-set coefficients (enables the eloc_partial and
     eloc_self checks)."""
     rep.samples += 1
     K = int(taps.K)
-    rc = taps.codes[..., 0].reshape(-1, K, T)
-    gc = np.asarray(gpu_codes).reshape(-1, K, T)
-    gaps = taps.gaps.reshape(-1, K, T)
+    H = taps.codes.shape[-1]
+    rc = taps.codes.reshape(-1, K, T, H)
+    gc = np.asarray(gpu_codes).reshape(-1, K, T, H)
+    gaps = taps.gaps.reshape(-1, K, T)  # min over the VQ heads
     L = rc.shape[0]
-    rep.locations += rc.size
+    rep.locations += gaps.size
     rep.flagged_locations += int((gaps < GAP_FLAG).sum())
-    mm = rc != gc
+    mm = (rc != gc).any(axis=-1)
     first = np.full(K, L)
     for b in range(L):
         live = mm[b] & (first[:, None] >= b)
