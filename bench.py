@@ -179,6 +179,58 @@ def cpu_baseline(w, seconds_target=20.0):
                       f"{cores} threads, reference double arithmetic"}
 
 
+def measure_device(torch, dist, eng, host_cfg, comm, steps, warmup, ws, local, flush):
+    """Device-timed steps on inputs resident in HBM: each step is one
+    local-energy pass over the rank's batch plus the fill_stats allreduce
+    (C ABI, NCCL). CUDA events on the engine's stream bracket each step, with
+    an L2 flush between steps; the time is the max over ranks.
+    Returns (ms_per_step, evals_per_rank_step, ledger of one step, summed
+    profile, one step's profile, launches per step)."""
+    import paper_2212_11296_b200 as P
+    B = host_cfg.shape[0]
+    pinned = torch.from_numpy(host_cfg).pin_memory()
+    d_cfg = pinned.to(f"cuda:{local}")
+    d_e = torch.empty(B, dtype=torch.float64, device=f"cuda:{local}")
+    d_l = torch.empty(B, dtype=torch.float64, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        led = eng.local_energies_device(d_cfg, d_e, d_l, stream)
+        eng.fill_stats_device(d_e, comm, stream)  # fill_stats: the one collective
+        return led
+
+    for _ in range(max(warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    led = step()  # ledger / evals of one step
+    torch.cuda.synchronize()
+    prof_one = eng.last_profile()
+    launches = eng.last_launch_count()
+    T = eng.cfg.seq_len
+    evals = led.other // T  # ledger 'other' = K*T per sample
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    prof = np.zeros(12)
+    for i in range(steps):
+        flush.zero_()  # L2 flush between timed steps (256 MB > 126 MB L2)
+        ev0[i].record(stream)
+        step()
+        ev1[i].record(stream)
+        prof += eng.last_profile()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    t_ms = float(np.sum([a.elapsed_time(b) for a, b in zip(ev0, ev1)]))
+    if ws > 1:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    return t_ms / steps, evals, led, prof, prof_one, launches
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -193,6 +245,10 @@ def main():
     ap.add_argument("--no-dense", action="store_true",
                     help="skip the no-reuse (dense) regime measurement")
     ap.add_argument("--batch", type=int, default=0, help="override samples per rank")
+    ap.add_argument("--also", default="c5",
+                    help="other workloads to device-time in the same run (comma list, or none)")
+    ap.add_argument("--no-strong", action="store_true",
+                    help="skip the strong-scaling measurement (N > 1)")
     args = ap.parse_args()
     rank, local, ws = dist_init()
     if args.impl == "reference":
@@ -213,57 +269,23 @@ def main():
     eng = P.LocalEnergyEngine(model, P.HamiltonianModel(lat), precision=w.precision,
                               device=local)
     host_cfg = P.zero_sz_samples(w.n_sites, rank * B, B, w.sample_seed)
-    pinned = torch.from_numpy(host_cfg).pin_memory()
-    d_cfg = pinned.to(f"cuda:{local}")
-    d_e = torch.empty(B, dtype=torch.float64, device=f"cuda:{local}")
-    d_l = torch.empty(B, dtype=torch.float64, device=f"cuda:{local}")
-    stream = torch.cuda.current_stream()
     flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=f"cuda:{local}")
+    # the fill_stats allreduce runs in the engine's C ABI over its own NCCL
+    # communicator (vqnqs_comm_*); torch.distributed only shares the NCCL id
+    # and the barriers / max-over-ranks timing
+    comm = None
+    if ws > 1:
+        from paper_2212_11296_b200.distributed import NcclComm
+        comm = NcclComm(rank, ws, local)
 
-    from paper_2212_11296_b200.distributed import allreduce_stats
-
-    def step():
-        led = eng.local_energies_device(d_cfg, d_e, d_l, stream)
-        # fill_stats (proj/src/trainer.cpp:184-198) over all ranks: the only
-        # collective (two small fp64 allreduces, NCCL over NVLink)
-        est = allreduce_stats(d_e)
-        return led, est
-
-    for _ in range(max(args.warmup, 0)):
-        step()
-    torch.cuda.synchronize()
-    led, v = step()  # ledger / evals of one step
-    torch.cuda.synchronize()
-    prof_one = eng.last_profile()
-    launches_per_step = eng.last_launch_count()
-    evals = led.other // w.model.seq_len  # ledger 'other' = K*T per sample
     clocks = ClockSampler(local)
     clocks.start()
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    prof = np.zeros(12)
-    for i in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (256 MB > 126 MB L2)
-        ev0[i].record(stream)
-        step()
-        ev1[i].record(stream)
-        prof += eng.last_profile()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
-    t_ms = float(np.sum(step_ms))
-    if ws > 1:
-        t = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
-    ms_per_step = t_ms / args.steps
+    ms_per_step, evals, led, prof, prof_one, launches_per_step = measure_device(
+        torch, dist, eng, host_cfg, comm, args.steps, args.warmup, ws, local, flush)
     value = evals * ws / (ms_per_step / 1e3)
 
-    # e2e through the public host-buffer API (pinned host in, E/logpsi out)
+    # e2e through the public host-buffer API: estimate_energy (pinned-staged
+    # host configs in, per-sample E/logpsi and the global statistics out)
     e2e_times = []
     for i in range(max(2, min(args.steps, 5))):
         if ws > 1:
@@ -271,8 +293,7 @@ def main():
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        e_host, l_host = eng.local_energies(host_cfg)
-        est_host = allreduce_stats(e_host, device=f"cuda:{local}")
+        est_host = eng.estimate_energy(host_cfg, comm)
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = float(np.median(e2e_times))
     if ws > 1:
@@ -280,6 +301,23 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     clk = clocks.stop()
+
+    # strong scaling beside the weak-scaling headline: the workload's FIXED
+    # batch split over the ranks by connected-set size (K-balanced shards,
+    # SURVEY 8(e)); shows the per-GPU underfill as N grows
+    strong = None
+    if ws > 1 and not args.no_strong:
+        from paper_2212_11296_b200.distributed import balanced_shards
+        glob = P.zero_sz_samples(w.n_sites, 0, w.batch, w.sample_seed)
+        owner = balanced_shards(glob, lat.bonds, ws)
+        mine = glob[owner == rank]
+        s_ms, s_evals, *_ = measure_device(torch, dist, eng, mine, comm, max(2, args.steps // 2),
+                                           1, ws, local, flush)
+        tot = torch.tensor([float(s_evals)], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tot)
+        strong = {"value": float(tot.item()) / (s_ms / 1e3), "unit": UNIT,
+                  "global_batch": w.batch, "samples_this_rank": int(mine.shape[0]),
+                  "ms_per_step": s_ms, "sharding": "K-balanced (vqnqs_balanced_shards)"}
 
     # the autoregressive sampler on the GPU (VqTransformer::sample,
     # proj/src/model.cpp:485-525): B draws, host in/out
@@ -314,22 +352,7 @@ def main():
     dense = None
     if not args.no_dense:
         eng.set_reuse(False)
-        step()
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        flush.zero_()
-        e0.record(stream)
-        step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        d_ms = e0.elapsed_time(e1)
-        if ws > 1:
-            t = torch.tensor([d_ms], dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            d_ms = float(t.item())
+        d_ms, *_ = measure_device(torch, dist, eng, host_cfg, comm, 1, 1, ws, local, flush)
         eng.set_reuse(True)
         dense = {"value": evals * ws / (d_ms / 1e3), "unit": UNIT, "ms_per_step": d_ms,
                  "steps": 1, "warmup": 1,
@@ -405,11 +428,40 @@ def main():
         "e2e": {"value": evals * ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(B * w.n_sites),
                 "d2h_bytes_per_step": int(2 * B * 8)},
         "gpu_launches": int(launches_per_step * args.steps),
+        "strong_scaling": strong,
         "no_reuse": dense,
         "sampler": sampler,
         "vmc_gradient": gradient,
         "clocks": clk,
     }
+    # the other bf16 workloads of BASELINE.json, device-timed the same way
+    # (c5 is the largest by algorithmic FLOPs per sample; c4 by evaluations)
+    eng.close()
+    others = {}
+    for name in [x for x in args.also.split(",") if x and x != "none"]:
+        wo = workload(name)
+        if wo.name == w.name:
+            continue
+        mo = P.VqTransformer.init(wo.model, wo.weight_seed, snap_bf16=wo.precision == "bf16")
+        lo = P.build_lattice("grid2d", (wo.L, wo.L), periodic=True)
+        eo = P.LocalEnergyEngine(mo, P.HamiltonianModel(lo), precision=wo.precision,
+                                 device=local)
+        co = P.zero_sz_samples(wo.n_sites, rank * wo.batch, wo.batch, wo.sample_seed)
+        o_ms, o_evals, o_led, o_prof, o_one, _ = measure_device(
+            torch, dist, eo, co, comm, max(2, args.steps // 2), 2, ws, local, flush)
+        ot = o_prof[7] / 1e3
+        o_attn_bytes = o_prof[4] * 6.0 * wo.model.d_hidden + o_prof[3] * (
+            4.0 * wo.model.d_hidden + 8.0)
+        nsteps = max(2, args.steps // 2)
+        others[wo.name] = {
+            "value": o_evals * ws / (o_ms / 1e3), "unit": UNIT, "ms_per_step": o_ms,
+            "steps": nsteps, "samples_per_rank": wo.batch, "precision": wo.precision,
+            "attention_roofline": {**roof(o_prof[9] / nsteps, o_attn_bytes / nsteps, ot / nsteps),
+                                   "share_of_step": (o_prof[7] / nsteps) / o_ms},
+            "f_alg_fraction_of_peak": (falg(wo, o_led, o_one) / (o_ms / 1e3) / 1e12) / tpk,
+            "dedup_savings": o_led.savings()[0]}
+        eo.close()
+    out["other_workloads"] = others
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline(w)
@@ -417,6 +469,8 @@ def main():
             out["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.close()
     if ws > 1:
         dist.destroy_process_group()
 

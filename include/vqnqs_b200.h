@@ -183,6 +183,44 @@ int vqnqs_gpu_taps(vqnqs_handle* h, const uint8_t* configs, int64_t B,
                    int32_t* K, int64_t* U, int32_t* codes, int64_t codes_cap,
                    double* lp_rows, int64_t lp_cap);
 
+/* ---- multi-GPU statistics (one process per GPU) ---- */
+
+/* An NCCL communicator over the ranks of one job. Rank 0 calls
+ * vqnqs_comm_unique_id and shares the VQNQS_COMM_ID_BYTES bytes out of band
+ * (MPI, torch.distributed, a file); every rank then calls vqnqs_comm_create
+ * with its rank and the CUDA device of its engine. */
+typedef struct vqnqs_comm vqnqs_comm;
+#define VQNQS_COMM_ID_BYTES 128
+int vqnqs_comm_unique_id(char* id);
+int vqnqs_comm_create(const char* id, int world, int rank, int device, vqnqs_comm** out);
+int vqnqs_comm_destroy(vqnqs_comm* c);
+
+/* estimate_energy's statistics (proj/src/trainer.cpp:200-211 and fill_stats,
+ * :184-198) over a batch sharded by sample across the ranks of `comm`: each
+ * rank passes its own B configurations (host); stats = {energy (mean Re E),
+ * variance (unbiased, two-pass), std_err = sqrt(variance / k), k} over ALL
+ * ranks' samples; e_re / logpsi (host [B], nullable) are this rank's; the
+ * ledger (nullable) is ADDED the whole job's ledger. The sums are fp64 on the
+ * device in a fixed order plus one NCCL allreduce per pass (the only
+ * data-path collective). comm = NULL: this process alone. A non-finite E_loc
+ * on any rank makes every rank return VQNQS_NUMERIC_ERROR. */
+int vqnqs_gpu_estimate_energy(vqnqs_handle* h, vqnqs_comm* comm, const uint8_t* configs,
+                              int64_t B, double* e_re, double* logpsi, int64_t* ledger7,
+                              double* stats);
+
+/* The same statistics for local energies already on the device (d_e_re [B],
+ * this rank's shard, e.g. from vqnqs_gpu_local_energies_device), ordered on
+ * `stream` (NULL = the handle's stream); synchronous. */
+int vqnqs_gpu_fill_stats_device(vqnqs_handle* h, vqnqs_comm* comm, const double* d_e_re,
+                                int64_t B, double* stats, void* stream);
+
+/* Balanced sample shards: owner[i] = the rank that evaluates
+ * sample i, dealing samples in decreasing connected-set size
+ * K = 1 + #antiparallel bonds to the rank with the least total K so far, so
+ * every rank gets about the same number of evaluations. */
+int vqnqs_balanced_shards(const uint8_t* configs, int64_t B, int n_sites, const int32_t* bonds,
+                          int nb, int world, int32_t* owner);
+
 /* Kernel launches issued by the last local-energies call (own kernels only). */
 int64_t vqnqs_gpu_last_launch_count(vqnqs_handle* h);
 

@@ -51,6 +51,16 @@ SIGNATURES = {
     "vqnqs_gpu_set_hamiltonian": (C.c_int, [C.c_void_p, P_I32, C.c_int, C.c_int, C.c_int]),
     "vqnqs_gpu_set_reuse": (C.c_int, [C.c_void_p, C.c_int]),
     "vqnqs_gpu_set_micro_batch": (C.c_int, [C.c_void_p, C.c_int]),
+    "vqnqs_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "vqnqs_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                    C.POINTER(C.c_void_p)]),
+    "vqnqs_comm_destroy": (C.c_int, [C.c_void_p]),
+    "vqnqs_gpu_estimate_energy": (C.c_int, [C.c_void_p, C.c_void_p, P_U8, C.c_int64, P_F64,
+                                            P_F64, P_I64, P_F64]),
+    "vqnqs_gpu_fill_stats_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                              P_F64, C.c_void_p]),
+    "vqnqs_balanced_shards": (C.c_int, [P_U8, C.c_int64, C.c_int, P_I32, C.c_int, C.c_int,
+                                        P_I32]),
     "vqnqs_grad_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "vqnqs_grad_log_prob": (C.c_int, [C.c_void_p, P_U8, C.c_int64, P_F64, C.c_double, P_F64,
                                       P_F64]),

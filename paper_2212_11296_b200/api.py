@@ -328,6 +328,44 @@ class LocalEnergyEngine:
         location computed."""
         N.check(N.lib().vqnqs_gpu_set_reuse(self._h, int(bool(reuse))))
 
+    def estimate_energy(self, batch, comm=None, ledger: Optional[Ledger] = None):
+        """fill_stats of estimate_energy (proj/src/trainer.cpp:184-211) over
+        this rank's shard `batch`, reduced over every rank of `comm` (a
+        distributed.NcclComm; None = this process alone) on the device.
+        Returns a VmcEstimate whose energy / variance / std_err are global and
+        whose local_energies are this rank's; `ledger` is added the whole
+        job's ledger."""
+        cfgs = np.ascontiguousarray(batch, np.uint8)
+        if cfgs.ndim != 2 or cfgs.shape[1] != self.cfg.n_sites:
+            raise ShapeError("configuration size != site count")
+        B = cfgs.shape[0]
+        e_re = np.zeros(B)
+        lpsi = np.zeros(B)
+        led = np.zeros(7, np.int64)
+        st = np.zeros(4)
+        N.check(N.lib().vqnqs_gpu_estimate_energy(
+            self._h, comm.handle if comm is not None else None, N.ptr(cfgs, C.c_uint8), B,
+            N.ptr(e_re, C.c_double), N.ptr(lpsi, C.c_double), N.ptr(led, C.c_int64),
+            N.ptr(st, C.c_double)))
+        if ledger is not None:
+            ledger += Ledger.from_array(led)
+        est = VmcEstimate(float(st[0]), float(st[1]), float(st[2]), e_re + 0j)
+        est.k_total = int(st[3])
+        est.logpsi = lpsi
+        return est
+
+    def fill_stats_device(self, d_e, comm=None, stream=None) -> "VmcEstimate":
+        """fill_stats over device-resident local energies (a torch float64
+        tensor, this rank's shard), global over `comm`'s ranks."""
+        st = np.zeros(4)
+        N.check(N.lib().vqnqs_gpu_fill_stats_device(
+            self._h, comm.handle if comm is not None else None, C.c_void_p(d_e.data_ptr()),
+            d_e.shape[0], N.ptr(st, C.c_double),
+            C.c_void_p(stream.cuda_stream) if stream is not None else None))
+        est = VmcEstimate(float(st[0]), float(st[1]), float(st[2]), np.zeros(0, complex))
+        est.k_total = int(st[3])
+        return est
+
     def set_micro_batch(self, samples: int) -> None:
         """Samples per micro-batch (0 = sized from the working-set budget)."""
         N.check(N.lib().vqnqs_gpu_set_micro_batch(self._h, int(samples)))

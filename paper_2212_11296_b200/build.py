@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libvqnqs_b200.so")
-SOURCES = ["engine.cu", "grad.cu", "capi.cpp", "host_model.cpp"]
+SOURCES = ["engine.cu", "grad.cu", "capi.cpp", "host_model.cpp", "comm.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for r in ex.map(lambda c: subprocess.run(c, check=True), cmds):
             pass
     tmp = LIB + ".tmp"
-    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcublas"],
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcublas", "-ldl"],
                    check=True)
     os.replace(tmp, LIB)
     return LIB

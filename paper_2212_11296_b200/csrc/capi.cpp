@@ -2,11 +2,13 @@
 // engine. Mirrors how the reference surfaces failures (typed exceptions,
 // proj/include/vqnqs/common.hpp:14-28) as integer status codes plus a
 // thread-local message.
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <vector>
 #include <string>
 
+#include "comm.h"
 #include "engine.h"
 
 struct vqnqs_handle {
@@ -14,6 +16,9 @@ struct vqnqs_handle {
 };
 struct vqnqs_grad_handle {
   vqb::GradEngine* g;
+};
+struct vqnqs_comm {
+  vqb::Comm* c;
 };
 
 namespace {
@@ -217,6 +222,88 @@ int vqnqs_gpu_taps(vqnqs_handle* h, const uint8_t* configs, int64_t B, int32_t* 
     t.lp_cap = lp_cap;
     std::vector<double> e(static_cast<size_t>(B)), lpsi(static_cast<size_t>(B));
     h->eng->run_host(configs, B, e.data(), nullptr, lpsi.data(), nullptr, &t);
+  });
+}
+
+int vqnqs_comm_unique_id(char* id) {
+  return guarded([&] {
+    if (!id) throw vqb::UsageError("null argument");
+    static_assert(NCCL_UNIQUE_ID_BYTES == VQNQS_COMM_ID_BYTES, "id size");
+    vqb::Comm::unique_id(id);
+  });
+}
+
+int vqnqs_comm_create(const char* id, int world, int rank, int device, vqnqs_comm** out) {
+  return guarded([&] {
+    if (!id || !out) throw vqb::UsageError("null argument");
+    *out = nullptr;
+    auto* c = new vqnqs_comm{nullptr};
+    try {
+      c->c = new vqb::Comm(id, world, rank, device);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int vqnqs_comm_destroy(vqnqs_comm* c) {
+  return guarded([&] {
+    if (!c) return;
+    delete c->c;
+    delete c;
+  });
+}
+
+int vqnqs_gpu_estimate_energy(vqnqs_handle* h, vqnqs_comm* comm, const uint8_t* configs,
+                              int64_t B, double* e_re, double* logpsi, int64_t* ledger7,
+                              double* stats) {
+  return guarded([&] {
+    if (!h || !stats || (!configs && B > 0)) throw vqb::UsageError("null argument");
+    if (B < 0) throw vqb::ConfigError("negative batch size");
+    const int n = h->eng->desc().n_sites;
+    for (int64_t i = 0; i < B * n; ++i)
+      if (configs[i] > 1) throw vqb::ConfigError("configuration entries must be 0 or 1");
+    h->eng->estimate(configs, B, e_re, logpsi, ledger7, comm ? comm->c : nullptr, stats);
+  });
+}
+
+int vqnqs_gpu_fill_stats_device(vqnqs_handle* h, vqnqs_comm* comm, const double* d_e_re,
+                                int64_t B, double* stats, void* stream) {
+  return guarded([&] {
+    if (!h || !stats || (!d_e_re && B > 0)) throw vqb::UsageError("null argument");
+    h->eng->fill_stats_device(d_e_re, B, comm ? comm->c : nullptr, stream, stats);
+  });
+}
+
+int vqnqs_balanced_shards(const uint8_t* configs, int64_t B, int n_sites, const int32_t* bonds,
+                          int nb, int world, int32_t* owner) {
+  return guarded([&] {
+    if ((!configs && B > 0) || (!bonds && nb > 0) || !owner) throw vqb::UsageError("null argument");
+    if (world < 1) throw vqb::ConfigError("world size must be >= 1");
+    // K_s = 1 + antiparallel bonds (the connected-set size, proj/src/hamiltonian.cpp:58-72)
+    std::vector<std::pair<int, int64_t>> k(static_cast<size_t>(B));
+    for (int64_t i = 0; i < B; ++i) {
+      int K = 1;
+      const uint8_t* c = configs + i * n_sites;
+      for (int b = 0; b < nb; ++b) K += c[bonds[2 * b]] != c[bonds[2 * b + 1]];
+      k[static_cast<size_t>(i)] = {K, i};
+    }
+    // longest-processing-time first: decreasing K (ties: batch order) to the
+    // rank with the least total so far (ties: lower rank)
+    std::stable_sort(k.begin(), k.end(),
+                     [](const std::pair<int, int64_t>& a, const std::pair<int, int64_t>& b) {
+                       return a.first > b.first;
+                     });
+    std::vector<int64_t> load(static_cast<size_t>(world), 0);
+    for (const auto& e : k) {
+      int r = 0;
+      for (int q = 1; q < world; ++q)
+        if (load[q] < load[r]) r = q;
+      load[r] += e.first;
+      owner[e.second] = r;
+    }
   });
 }
 

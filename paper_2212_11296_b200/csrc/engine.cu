@@ -22,6 +22,7 @@
 #include <sstream>
 #include <vector>
 
+#include "comm.h"
 #include "common.cuh"
 #include "engine.h"
 #include "pipeline_kernels.cuh"
@@ -396,6 +397,7 @@ class EngineImpl {
       if (e) cudaEventDestroy(e);
     for (auto& e : lev)
       if (e) cudaEventDestroy(e);
+    red_.release();
     if (own) cudaStreamDestroy(own);
     if (h_pinned_cfg) cudaFreeHost(h_pinned_cfg);
     if (h_pinned_out) cudaFreeHost(h_pinned_out);
@@ -1056,6 +1058,104 @@ class EngineImpl {
       if (logpsi) logpsi[i] = h_pinned_out[B + i];
     }
   }
+
+  // fill_stats over a device-resident shard e[B] (fp64, fixed order) into
+  // red[0..3] (n, sum, #non-finite, centred sum of squares) and, when led is
+  // given, the ledger into red[4..10] (int64); with comm every quantity is
+  // summed over the ranks (NCCL on stream st). Asynchronous.
+  void stats_device(const double* e, int64_t B, Comm* comm, cudaStream_t st, double* red,
+                    const int64_t* led) {
+    k_stats<<<1, 1024, 0, st>>>(B, e, red, 0);
+    if (comm) comm->allreduce_f64(red, 3, st);
+    k_stats<<<1, 1024, 0, st>>>(B, e, red, 1);
+    if (comm) comm->allreduce_f64(red + 3, 1, st);
+    launches += 2;
+    if (led) {
+      int64_t* dled = reinterpret_cast<int64_t*>(red + 4);
+      CK(cudaMemcpyAsync(dled, led, VQNQS_LEDGER_SLOTS * sizeof(int64_t),
+                         cudaMemcpyHostToDevice, st));
+      if (comm) comm->allreduce_i64(dled, VQNQS_LEDGER_SLOTS, st);
+    }
+  }
+
+  // fill_stats of a device-resident shard (the device-buffer estimate):
+  // stats = {energy, variance, std_err, k}; synchronous on st.
+  DBuf<double> red_;
+  void fill_stats_device(const double* e, int64_t B, Comm* comm, cudaStream_t st,
+                         double* stats) {
+    CK(cudaSetDevice(dev));
+    red_.ensure(16);
+    stats_device(e, B, comm, st, red_.p, nullptr);
+    double hr[4];
+    CK(cudaMemcpyAsync(hr, red_.p, sizeof(hr), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hr[2] > 0) throw NumericError("non-finite local energy in the batch");
+    finish_stats(hr, stats);
+  }
+  static void finish_stats(const double* hr, double* stats) {
+    const int64_t k = int64_t(hr[0] + 0.5);
+    if (k < 1) throw ConfigError("k_samples must be >= 1");
+    const double var = k > 1 ? hr[3] / double(k - 1) : 0.0;
+    stats[0] = hr[1] / hr[0];
+    stats[1] = var;
+    stats[2] = std::sqrt(var / double(k));
+    stats[3] = double(k);
+  }
+
+  // estimate_energy's statistics (proj/src/trainer.cpp:200-211 with
+  // fill_stats, :184-198) over this rank's shard; with a communicator the
+  // sums, the non-finite count and the ledger are reduced over all ranks
+  // (NCCL, on the engine stream), so every rank returns the global estimate.
+  void estimate(const uint8_t* configs, int64_t B, double* e_re, double* logpsi,
+                int64_t* ledger7, Comm* comm, double* stats) {
+    CK(cudaSetDevice(dev));
+    if (comm && comm->device() != dev)
+      throw UsageError("communicator and engine are on different devices");
+    const size_t nbytes = size_t(B) * N;
+    if (h_pinned_cfg_n < nbytes) {
+      if (h_pinned_cfg) cudaFreeHost(h_pinned_cfg);
+      CK(cudaMallocHost(&h_pinned_cfg, std::max<size_t>(nbytes, 1)));
+      h_pinned_cfg_n = nbytes;
+    }
+    if (h_pinned_out_n < size_t(2 * B + 16)) {
+      if (h_pinned_out) cudaFreeHost(h_pinned_out);
+      CK(cudaMallocHost(&h_pinned_out, (2 * B + 16) * sizeof(double)));
+      h_pinned_out_n = 2 * B + 16;
+    }
+    if (nbytes) std::memcpy(h_pinned_cfg, configs, nbytes);
+    cfg_stage_.ensure(std::max<size_t>(nbytes, 1));
+    out_stage_.ensure(2 * B + 16);
+    double* red = out_stage_.p + 2 * B;  // [4] sums, then [8] ledger (int64)
+    int64_t led[VQNQS_LEDGER_SLOTS] = {0, 0, 0, 0, 0, 0, 0};
+    if (B > 0) {
+      CK(cudaMemcpyAsync(cfg_stage_.p, h_pinned_cfg, nbytes, cudaMemcpyHostToDevice, own));
+      run_device(cfg_stage_.p, B, out_stage_.p, out_stage_.p + B, led, own, nullptr);
+    }
+    stats_device(out_stage_.p, B, comm, own, red, led);
+    CK(cudaMemcpyAsync(h_pinned_out, out_stage_.p, (2 * B + 4 + VQNQS_LEDGER_SLOTS) *
+                       sizeof(double), cudaMemcpyDeviceToHost, own));
+    CK(cudaStreamSynchronize(own));
+    const double* hr = h_pinned_out + 2 * B;
+    for (int64_t i = 0; i < B; ++i) {
+      const double e = h_pinned_out[i];
+      if (!std::isfinite(e)) {
+        std::string s;
+        for (int j = 0; j < N; ++j) s.push_back(configs[i * N + j] ? '1' : '0');
+        throw NumericError("non-finite local energy at configuration " + s);
+      }
+    }
+    if (hr[2] > 0)  // every rank learns of it through the reduced count
+      throw NumericError("non-finite local energy on another rank");
+    for (int64_t i = 0; i < B; ++i) {
+      if (e_re) e_re[i] = h_pinned_out[i];
+      if (logpsi) logpsi[i] = h_pinned_out[B + i];
+    }
+    finish_stats(hr, stats);
+    if (ledger7) {
+      const int64_t* gl = reinterpret_cast<const int64_t*>(hr + 4);
+      for (int i = 0; i < VQNQS_LEDGER_SLOTS; ++i) ledger7[i] += gl[i];
+    }
+  }
 };
 
 Engine::Engine(const vqnqs_model_desc& d, const double* const* params, int n_params, int precision,
@@ -1064,6 +1164,15 @@ Engine::Engine(const vqnqs_model_desc& d, const double* const* params, int n_par
 Engine::~Engine() { delete p_; }
 void Engine::set_reuse(bool reuse) { p_->set_reuse(reuse); }
 void Engine::set_micro_batch(int samples) { p_->set_micro_batch(samples); }
+void Engine::fill_stats_device(const double* d_e, int64_t B, Comm* comm, void* stream,
+                               double* stats) {
+  p_->fill_stats_device(d_e, B, comm, stream ? static_cast<cudaStream_t>(stream) : p_->own,
+                        stats);
+}
+void Engine::estimate(const uint8_t* configs, int64_t B, double* e_re, double* logpsi,
+                      int64_t* ledger7, Comm* comm, double* stats) {
+  p_->estimate(configs, B, e_re, logpsi, ledger7, comm, stats);
+}
 void Engine::set_hamiltonian(const int32_t* bonds, int nb, int n_sites, bool marshall) {
   p_->set_hamiltonian(bonds, nb, n_sites, marshall);
 }

@@ -61,6 +61,7 @@ void ledger_add(const vqnqs_model_desc& c, int64_t K, const int64_t* U, int64_t*
 
 class EngineImpl;
 class GradImpl;
+class Comm;
 
 // d/dtheta sum_i w_i log P(s_i) on the GPU
 // (proj/src/trainer.cpp:213-246 backward through build_log_prob,
@@ -101,6 +102,14 @@ class Engine {
   // host (added to), may be null. taps optional (host buffers).
   void run_device(const uint8_t* d_configs, int64_t B, double* d_e, double* d_logpsi,
                   int64_t* ledger7, void* stream, Taps* taps);
+  // estimate_energy / fill_stats over this rank's shard (host configs);
+  // with comm the statistics and ledger are global over all ranks.
+  // stats = {energy, variance, std_err, k_total}.
+  void estimate(const uint8_t* configs, int64_t B, double* e_re, double* logpsi,
+                int64_t* ledger7, Comm* comm, double* stats);
+  // fill_stats of device-resident local energies d_e[B] (this rank's
+  // shard), global over comm's ranks; synchronous on `stream`.
+  void fill_stats_device(const double* d_e, int64_t B, Comm* comm, void* stream, double* stats);
   // Host batch (pinned staging inside).
   void run_host(const uint8_t* configs, int64_t B, double* e_re, double* e_im, double* logpsi,
                 int64_t* ledger7, Taps* taps);

@@ -749,4 +749,49 @@ __global__ void k_eloc(int S, int R1, int T, int g, int V, double coeff,
   }
 }
 
+// fill_stats (proj/src/trainer.cpp:184-198) over a device-resident shard of
+// local energies, in a fixed summation order (deterministic). One CTA of
+// 1024 threads; each thread sums a contiguous slice, then a fixed tree.
+//   mode 0: red[0] = n, red[1] = sum Re E, red[2] = #non-finite
+//   mode 1: red[3] = sum (Re E - red[1] / red[0])^2, after red[0..2] have
+//           been summed over the ranks (the reference's two-pass variance)
+__global__ void __launch_bounds__(1024) k_stats(int64_t n, const double* __restrict__ e,
+                                                double* __restrict__ red, int mode) {
+  __shared__ double sh[1024];
+  __shared__ double bad[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t b = tid * per, en = min(n, b + per);
+  const double mean = mode == 1 ? red[1] / red[0] : 0.0;
+  double acc = 0.0, nf = 0.0;
+  for (int64_t i = b; i < en; ++i) {
+    const double v = e[i];
+    if (mode == 0) {
+      if (isfinite(v)) acc += v;
+      else nf += 1.0;
+    } else if (isfinite(v)) {
+      acc += (v - mean) * (v - mean);
+    }
+  }
+  sh[tid] = acc;
+  bad[tid] = nf;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (tid < o) {
+      sh[tid] += sh[tid + o];
+      bad[tid] += bad[tid + o];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (mode == 0) {
+      red[0] = double(n);
+      red[1] = sh[0];
+      red[2] = bad[0];
+    } else {
+      red[3] = sh[0];
+    }
+  }
+}
+
 }  // namespace vqb

@@ -59,6 +59,55 @@ def allreduce_stats(e_local, device=None, group=None) -> VmcEstimate:
                        np.zeros(0, complex))
 
 
+def balanced_shards(configs, bonds, world: int) -> np.ndarray:
+    """owner[i] = rank of sample i, balancing the connected-set sizes
+    K = 1 + #antiparallel bonds across ranks; the native
+    vqnqs_balanced_shards, deterministic on every rank."""
+    import ctypes as C
+    from . import _native as N
+    cfgs = np.ascontiguousarray(configs, np.uint8)
+    b = np.ascontiguousarray(bonds, np.int32)
+    owner = np.zeros(cfgs.shape[0], np.int32)
+    N.check(N.lib().vqnqs_balanced_shards(N.ptr(cfgs, C.c_uint8), cfgs.shape[0], cfgs.shape[1],
+                                          N.ptr(b, C.c_int32), b.shape[0], int(world),
+                                          N.ptr(owner, C.c_int32)))
+    return owner
+
+
+class NcclComm:
+    """The native NCCL communicator (vqnqs_comm_*) of one rank: rank 0's
+    unique id is shared over torch.distributed (any backend), then each rank
+    joins with the CUDA device of its engine. Used by
+    LocalEnergyEngine.estimate_energy for the fill_stats allreduce."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import ctypes as C
+        import torch.distributed as dist
+        from . import _native as N
+        buf = C.create_string_buffer(128)
+        if rank == 0:
+            N.check(N.lib().vqnqs_comm_unique_id(buf))
+        ids = [buf.raw]
+        if world > 1:
+            dist.broadcast_object_list(ids, src=0, group=group)
+        h = C.c_void_p()
+        N.check(N.lib().vqnqs_comm_create(ids[0], world, rank, device, C.byref(h)))
+        self.handle = h
+        self.rank, self.world, self.device = rank, world, device
+
+    def close(self):
+        from . import _native as N
+        if getattr(self, "handle", None):
+            N.lib().vqnqs_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def local_energies_sharded(engine, batch_global, rank: int, world: int,
                            group=None, device=None):
     """Evaluate this rank's shard of a global batch on `engine` (a
