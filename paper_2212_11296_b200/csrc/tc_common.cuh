@@ -159,6 +159,16 @@ __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// One lane of a converged warp (the same lane every time): the issuing lane
+// of warp-uniform tcgen05 code.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}\n"
+      : "=r"(p));
+  return p != 0;
+}
+
 // mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
@@ -179,6 +189,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
       "@!P bra WAIT_%=;\n\t}\n" ::"r"(a),
       "r"(phase), "r"(1000000u)
       : "memory");
+}
+
+// Off-critical-path waiter: polls with a back-off sleep so it does not take
+// issue slots from the warps sharing its scheduler.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t phase) {
+  const uint32_t a = smem_u32(b);
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(done)
+        : "r"(a), "r"(phase)
+        : "memory");
+    if (done) break;
+    __nanosleep(128);
+  }
 }
 
 // cp.async 16 bytes global -> shared (L2 only)
