@@ -396,43 +396,64 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   } else if (warp >= TCA_MMA_WARP) {
     // ================= MMA warp (one thread issues every tcgen05.mma)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
-    if (warp == TCA_MMA_WARP && lane == 0 && nit > 0) {
-      auto issue_scores = [&](int it, int hq, int kb_base) {
+    if (warp == TCA_MMA_WARP && nit > 0) {
+      // The whole warp runs the (warp-uniform) schedule and one elected lane
+      // issues, so descriptors stay in uniform registers and the MMA loops
+      // are unrolled: this thread's issue latency paces the tensor pipe
+      // (scripts/mma_probe2.cu: a 12-step value chain completes in ~270
+      // cycles when issued unrolled).
+      const bool leader = tc::elect_one();
+      auto own_of = [&](int j) {  // own key columns in use: 16 ceil(nloc / 16)
+        return (reinterpret_cast<const int32_t*>(slot(j) + 1544)[0] + 15) & ~15;
+      };
+      auto issue_scores = [&](int it, int hq, int kb_base, int nown) {
         const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
         const uint32_t qoff = (uint32_t)(hq * dh * 2);  // head offset inside the 128-B row
         const uint32_t idS_b = tc::make_idesc_bf16(128, kb_base > 0 ? kb_base : 16);
-        const uint32_t idS_o = tc::make_idesc_bf16(128, 128);
+        const uint32_t idS_o = tc::make_idesc_bf16(128, nown);
         const uint64_t dq = tc::make_desc_sw128(st + L.q + qoff);
         const uint64_t dkb = tc::make_desc_sw128(st + L.kbase + qoff);
         const uint64_t dko = tc::make_desc_sw128(st + L.kown + qoff);
-        for (int k = 0; k < dh / 16; ++k) {  // +32 B along K = +2 in the descriptor
-          if (kb_base > 0) tc::mma_bf16(tmem + TS_BASE, dq + 2 * k, dkb + 2 * k, idS_b, k != 0);
-          tc::mma_bf16(tmem + TS_OWN, dq + 2 * k, dko + 2 * k, idS_o, k != 0);
+        if (leader) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // +32 B along K = +2 in the descriptor
+            if (k < dh / 16) {
+              if (kb_base > 0) tc::mma_bf16(tmem + TS_BASE, dq + 2 * k, dkb + 2 * k, idS_b, k != 0);
+              tc::mma_bf16(tmem + TS_OWN, dq + 2 * k, dko + 2 * k, idS_o, k != 0);
+            }
+          }
+          tc::mma_commit(s_full);
         }
-        tc::mma_commit(s_full);
+        __syncwarp();
       };
-      auto issue_pv = [&](int it, int hh, int kb_base) {
+      auto issue_pv = [&](int it, int hh, int kb_base, int nown) {
         const uint32_t st = sb + (uint32_t)(it & 1) * L.stage;
         const uint32_t koff = (uint32_t)(hh * dh * 2);
         const uint32_t idO = tc::make_idesc_bf16(128, dh) | (1u << 16);
         const uint32_t tO = tmem + TS_O + (uint32_t)((it & 1) * 64 + hh * dh), tA = tmem + TS_P;
         const uint64_t db = tc::make_desc_sw128(st + L.vbase + koff);
         const uint64_t dw = tc::make_desc_sw128(st + L.vown + koff);
-        // descriptor start field is address >> 4: 16 key rows = +128
-        for (int k16 = 0; k16 < kb_base; k16 += 16)
-          tc::mma_bf16_ts(tO, tA + (uint32_t)(k16 >> 1), db + (uint64_t)(k16 * 8), idO,
-                          k16 > 0 ? 1u : 0u);
-        for (int k16 = 0; k16 < 128; k16 += 16)
-          tc::mma_bf16_ts(tO, tA + (uint32_t)((kb_base + k16) >> 1), dw + (uint64_t)(k16 * 8),
-                          idO, (kb_base > 0 || k16 > 0) ? 1u : 0u);
-        tc::mma_commit(pv_done);
+        const int nb16 = kb_base >> 4, no16 = nown >> 4;
+        if (leader) {
+          // descriptor start field is address >> 4: 16 key rows = +128
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (i < nb16) tc::mma_bf16_ts(tO, tA + 8u * i, db + 128u * i, idO, i > 0 ? 1u : 0u);
+          const uint32_t tAo = tA + (uint32_t)(kb_base >> 1);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (i < no16)
+              tc::mma_bf16_ts(tO, tAo + 8u * i, dw + 128u * i, idO, (nb16 > 0 || i > 0) ? 1u : 0u);
+          tc::mma_commit(pv_done);
+        }
+        __syncwarp();
       };
       uint32_t ph_free = 0, ph_p = 0;
       // S(0)
       tc::mbar_wait(&st_full[0], 0);
       tc::fence_after();
-      int kb_cur = kb_of(0);
-      issue_scores(0, 0, kb_cur);
+      int kb_cur = kb_of(0), no_cur = own_of(0);
+      issue_scores(0, 0, kb_cur, no_cur);
       int it = 0, hh = 0, j = 0, gi = 0;  // head g = (it, hh), item it = (j, gi)
       for (;;) {
         // next head (it2, hh2)
@@ -445,16 +466,17 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
             ++j2;
           }
         }
-        int kb_next = kb_cur;
+        int kb_next = kb_cur, no_next = no_cur;
         if (it2 < nit) {
           tc::mbar_wait(s_free, ph_free);  // every warp holds S(g)
           ph_free ^= 1;
           if (it2 != it) {
             tc::mbar_wait(&st_full[it2 & 1], (it2 >> 1) & 1);  // operands of item it2
             kb_next = kb_of(j2);
+            no_next = own_of(j2);
           }
           tc::fence_after();
-          issue_scores(it2, hh2, kb_next);
+          issue_scores(it2, hh2, kb_next, no_next);
         }
         if (hh == 0 && it >= 2) {
           tc::mbar_wait(&o_empty[it & 1], ((it - 2) >> 1) & 1);  // O buffer drained
@@ -462,14 +484,18 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         tc::mbar_wait(p_full, ph_p);  // every warp wrote P(g)
         ph_p ^= 1;
         tc::fence_after();
-        issue_pv(it, hh, kb_cur);
-        if (hh == hpg - 1) tc::mma_commit(&stage_free[it & 1]);  // item it's operands read
+        issue_pv(it, hh, kb_cur, no_cur);
+        if (hh == hpg - 1) {  // item it's operands read
+          if (leader) tc::mma_commit(&stage_free[it & 1]);
+          __syncwarp();
+        }
         if (it2 >= nit) break;
         it = it2;
         hh = hh2;
         j = j2;
         gi = gi2;
         kb_cur = kb_next;
+        no_cur = no_next;
       }
     }
     if (warp > TCA_MMA_WARP && nit > 0) {
