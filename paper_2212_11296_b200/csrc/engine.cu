@@ -560,7 +560,8 @@ class EngineImpl {
     // (d) input layer
     int32_t* Icur = I_a.p;
     int32_t* Inext = I_b.p;
-    k_dedup<0><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
+    smem_optin(reinterpret_cast<const void*>(k_dedup<0>), dedup_smem_bytes());
+    k_dedup<0><<<S, DEDUP_THREADS, dedup_smem_bytes(), st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
                                   slot_.p, lrow_.p, lpos_.p, tok0_.p, row_bond_.p, d_bonds, R1, T,
                                   g, V, nullptr, nullptr, int(dense), Icur, rep_of_.p, Ucnt_.p,
                                   nullptr);
@@ -658,7 +659,8 @@ class EngineImpl {
             ctup_.ensure(M);
             k_pack_codes<<<int((M + 255) / 256), 256, 0, st>>>(tot + 0, H, qbits, code_.p,
                                                                ctup_.p, nullptr);
-            k_dedup<2><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p,
+            smem_optin(reinterpret_cast<const void*>(k_dedup<2>), dedup_smem_bytes());
+            k_dedup<2><<<S, DEDUP_THREADS, dedup_smem_bytes(), st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p,
                                           tuid_.p, slot_.p, nullptr, nullptr, nullptr, nullptr,
                                           nullptr, R1, T, g, V, nullptr, nullptr, int(dense),
                                           ckey_.p, rep_of_.p, Uc_next, ctup_.p);
@@ -670,7 +672,8 @@ class EngineImpl {
           }
           ckey = ckey_.p;
         }
-        k_dedup<1><<<S, 512, 0, st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
+        smem_optin(reinterpret_cast<const void*>(k_dedup<1>), dedup_smem_bytes());
+        k_dedup<1><<<S, DEDUP_THREADS, dedup_smem_bytes(), st>>>(Mact_.p, act_off_.p, tab_off_.p, tkey_.p, trep_.p, tuid_.p,
                                       slot_.p, nullptr, nullptr, nullptr, nullptr, nullptr, R1, T,
                                       g, V, Icur, ckey, int(dense), Inext, rep_of_.p, Uc_next,
                                       nullptr);

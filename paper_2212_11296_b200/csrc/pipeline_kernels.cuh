@@ -296,12 +296,14 @@ __global__ void k_enumerate(int S, int R1, int T, const int32_t* __restrict__ K,
 //                         (H > 1: the code tuple packed or numbered, k_pack_codes)
 //   MODE 2 (H > 1, wide tuples): key = the packed code tuple itself; the ids
 //                         number the distinct tuples of the sample for MODE 1
-// One CTA per sample; open-addressing table in global memory (L2-resident),
-// atomicCAS claims a slot, atomicMin keeps the first location, a block scan
-// over locations in order assigns ids. Slots are reset before exit so the
-// table is clean for the next layer.
+// One CTA per sample; open-addressing table (atomicCAS claims a slot,
+// atomicMin keeps the first location), then a block scan over locations in
+// order assigns ids. The table lives in shared memory (k_dedup below); the
+// global-memory variant (dedup_global, L2-resident, slots reset before exit
+// so the table is clean for the next layer) takes the samples that do not
+// fit it.
 template <int MODE>
-__global__ void __launch_bounds__(512) k_dedup(
+__device__ void dedup_global(
     const int32_t* __restrict__ Mact, const int64_t* __restrict__ act_off,
     const int64_t* __restrict__ tab_off, unsigned long long* __restrict__ tkey,
     int32_t* __restrict__ trep, int32_t* __restrict__ tuid, int32_t* __restrict__ slot,
@@ -316,9 +318,9 @@ __global__ void __launch_bounds__(512) k_dedup(
     // outputs
     int32_t* __restrict__ I_out, int32_t* __restrict__ rep_of, int32_t* __restrict__ Ucnt,
     // MODE 2 input
-    const unsigned long long* __restrict__ tup) {
-  __shared__ int wtot[32];
-  __shared__ int run_s;
+    const unsigned long long* __restrict__ tup, int* sh_wtot, int* sh_run) {
+  int* wtot = sh_wtot;
+  int& run_s = *sh_run;
   const int s = blockIdx.x;
   const int M = Mact[s];
   const int64_t base = act_off[s];
@@ -409,6 +411,184 @@ __global__ void __launch_bounds__(512) k_dedup(
     tkey[tb + h] = VQB_EMPTY_KEY;
     trep[tb + h] = VQB_INT_MAX;
   }
+}
+
+// Key of location i of sample s (MODE 0: (p, BOS-shifted token); MODE 1:
+// (residual row, code); MODE 2: the packed code tuple).
+template <int MODE>
+__device__ __forceinline__ unsigned long long dedup_key(
+    int64_t loc, const int32_t* __restrict__ lrow, const int16_t* __restrict__ lpos,
+    const int32_t* __restrict__ tok0, const int32_t* __restrict__ row_bond,
+    const int32_t* __restrict__ bonds, int R1, int T, int g, int V,
+    const int32_t* __restrict__ I_in, const int32_t* __restrict__ code,
+    const unsigned long long* __restrict__ tup) {
+  if (MODE == 0) {
+    const int r = lrow[loc];
+    const int p = lpos[loc];
+    const int sidx = r / R1;
+    const int tok = p == 0 ? V : row_token(tok0 + (int64_t)sidx * T, bonds, row_bond[r], g, p - 1);
+    return (unsigned long long)p * (unsigned long long)(V + 1) + (unsigned long long)tok;
+  } else if (MODE == 1) {
+    return ((unsigned long long)(uint32_t)I_in[loc] << 32) | (uint32_t)code[loc];
+  } else {
+    return tup[loc];
+  }
+}
+
+// Shared-memory table: DEDUP_SC slots (key; first location, later -(id + 1))
+// and a 16-bit slot per location, so a sample's dedup touches HBM only for
+// its keys in and its ids out (~12 B per location instead of ~8 dependent
+// L2 round trips per location through a global table); 176 KB, one CTA of
+// 1024 threads per SM. A sample whose unique keys exceed half the slots, or whose locations
+// exceed DEDUP_SMAX, takes the global table path (dedup_global) instead;
+// MODE 0 keys index the table directly when the key space (T (V + 1)) fits.
+constexpr int DEDUP_SC = 8192;
+constexpr int DEDUP_SMAX = 40960;
+constexpr int DEDUP_THREADS = 1024;
+inline size_t dedup_smem_bytes() { return size_t(DEDUP_SC) * 12 + size_t(DEDUP_SMAX) * 2; }
+
+template <int MODE>
+__global__ void __launch_bounds__(DEDUP_THREADS, 1) k_dedup(
+    const int32_t* __restrict__ Mact, const int64_t* __restrict__ act_off,
+    const int64_t* __restrict__ tab_off, unsigned long long* __restrict__ tkey,
+    int32_t* __restrict__ trep, int32_t* __restrict__ tuid, int32_t* __restrict__ slot,
+    const int32_t* __restrict__ lrow, const int16_t* __restrict__ lpos,
+    const int32_t* __restrict__ tok0, const int32_t* __restrict__ row_bond,
+    const int32_t* __restrict__ bonds, int R1, int T, int g, int V,
+    const int32_t* __restrict__ I_in, const int32_t* __restrict__ code, int dense,
+    int32_t* __restrict__ I_out, int32_t* __restrict__ rep_of, int32_t* __restrict__ Ucnt,
+    const unsigned long long* __restrict__ tup) {
+  extern __shared__ __align__(16) uint8_t dd_smem[];
+  __shared__ int wtot[32];
+  __shared__ int run_s, n_new;
+  unsigned long long* skey = reinterpret_cast<unsigned long long*>(dd_smem);
+  int32_t* srep = reinterpret_cast<int32_t*>(skey + DEDUP_SC);
+  uint16_t* sslot = reinterpret_cast<uint16_t*>(srep + DEDUP_SC);
+  const int s = blockIdx.x;
+  const int M = Mact[s];
+  const int64_t base = act_off[s];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
+  if (dense) {  // no-reuse regime: every location is its own unique row
+    for (int i = tid; i < M; i += nt) {
+      I_out[base + i] = i;
+      rep_of[base + i] = i;
+    }
+    if (tid == 0) Ucnt[s] = M;
+    return;
+  }
+  const bool direct = MODE == 0 && T * (V + 1) <= DEDUP_SC;
+  if (M > DEDUP_SMAX) {
+    dedup_global<MODE>(Mact, act_off, tab_off, tkey, trep, tuid, slot, lrow, lpos, tok0,
+                       row_bond, bonds, R1, T, g, V, I_in, code, 0, I_out, rep_of, Ucnt, tup,
+                       wtot, &run_s);
+    return;
+  }
+  for (int h = tid; h < DEDUP_SC; h += nt) {
+    skey[h] = VQB_EMPTY_KEY;
+    srep[h] = VQB_INT_MAX;
+  }
+  if (tid == 0) n_new = 0;
+  __syncthreads();
+  // phase 1: insert (probing stops once the table is half full). Keys are
+  // loaded four locations ahead of their inserts so the global loads overlap.
+  constexpr int PF = 4;
+  for (int i0 = tid; i0 < M; i0 += PF * nt) {
+    unsigned long long keys[PF];
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      const int i = i0 + k * nt;
+      keys[k] = i < M ? dedup_key<MODE>(base + i, lrow, lpos, tok0, row_bond, bonds, R1, T, g, V,
+                                        I_in, code, tup)
+                      : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+    const int i = i0 + k * nt;
+    if (i >= M) break;
+    const unsigned long long key = keys[k];
+    int h;
+    if (direct) {
+      h = (int)key;
+    } else {
+      // 32-bit multiplicative hash of the two key halves (cheap; the
+      // table is small and probing is linear)
+      uint32_t hh = (uint32_t)key * 0x9E3779B1u ^ (uint32_t)(key >> 32) * 0x85EBCA6Bu;
+      h = (int)((hh ^ (hh >> 15)) & (DEDUP_SC - 1));
+      for (;;) {
+        const unsigned long long cur = skey[h];  // settled slots need no atomic
+        if (cur == key) break;
+        if (cur != VQB_EMPTY_KEY) {
+          h = (h + 1) & (DEDUP_SC - 1);
+          continue;
+        }
+        const unsigned long long prev = atomicCAS(&skey[h], VQB_EMPTY_KEY, key);
+        if (prev == key) break;
+        if (prev == VQB_EMPTY_KEY) {
+          atomicAdd(&n_new, 1);
+          break;
+        }
+        h = (h + 1) & (DEDUP_SC - 1);
+      }
+    }
+    if (srep[h] > i) atomicMin(&srep[h], i);  // later locations of a seen key skip it
+    sslot[i] = (uint16_t)h;
+    }
+    if (*reinterpret_cast<volatile int*>(&n_new) > DEDUP_SC / 2) break;
+  }
+  __syncthreads();
+  if (n_new > DEDUP_SC / 2) {  // too many distinct keys for the table
+    dedup_global<MODE>(Mact, act_off, tab_off, tkey, trep, tuid, slot, lrow, lpos, tok0,
+                       row_bond, bonds, R1, T, g, V, I_in, code, 0, I_out, rep_of, Ucnt, tup,
+                       wtot, &run_s);
+    return;
+  }
+  // phase 2: ids in first-occurrence order (warp w numbers the contiguous
+  // location segment [w L, (w + 1) L) after one block scan of warp counts)
+  const int nw = nt >> 5;
+  const int L = (M + nw - 1) / nw;
+  const int seg0 = min(M, w * L), seg1 = min(M, seg0 + L);
+  int mine = 0;
+  for (int i0 = seg0; i0 < seg1; i0 += 32) {
+    const int i = i0 + lane;
+    const bool flag = i < seg1 && srep[sslot[i]] == i;
+    mine += __popc(__ballot_sync(0xffffffffu, flag));
+  }
+  if (lane == 0) wtot[w] = mine;
+  __syncthreads();
+  if (w == 0) {
+    int v = lane < nw ? wtot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane < nw) wtot[lane] = v;  // inclusive
+    if (lane == 31) run_s = v;      // total
+  }
+  __syncthreads();
+  int next = w > 0 ? wtot[w - 1] : 0;
+  // a key's entry is written only by its first location, and no other
+  // location's test (srep[h] == i >= 0) can match the negative id
+  for (int i0 = seg0; i0 < seg1; i0 += 32) {
+    const int i = i0 + lane;
+    int h = 0;
+    bool flag = false;
+    if (i < seg1) {
+      h = sslot[i];
+      flag = srep[h] == i;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, flag);
+    if (flag) {
+      const int id = next + __popc(m & ((1u << lane) - 1u));
+      srep[h] = -(id + 1);
+      rep_of[base + id] = i;
+    }
+    next += __popc(m);
+  }
+  __syncthreads();
+  // phase 3: ids to locations
+  for (int i = tid; i < M; i += nt) I_out[base + i] = -srep[sslot[i]] - 1;
+  if (tid == 0) Ucnt[s] = run_s;
 }
 
 // Input embeddings of the unique input rows: tok_embed[tok] + pos_embed[p]
