@@ -21,6 +21,12 @@ int vqnqs_debug_tc_attention(int S, int R1, int T, int d, int nh, const int32_t*
                              const int64_t* row_aoff, const int64_t* act_off, int64_t M,
                              const int32_t* I, const int64_t* Uoff, const void* qkv, void* xh,
                              void* xl, float* xn2, float* rr2);
+/* Engine test hook: force the VQ code of every active location to the
+ * reference's (codes host [n_samples][L][nb+1][T] int16, rows in bond order,
+ * -1 = keep the computed code) for the following calls on batches of
+ * exactly n_samples; codes = NULL clears. vq_heads = 1. */
+typedef struct vqnqs_handle vqnqs_handle;
+int vqnqs_debug_set_code_override(vqnqs_handle* h, const int16_t* codes, int64_t n_samples);
 #ifdef __cplusplus
 }
 #endif

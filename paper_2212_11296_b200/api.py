@@ -366,6 +366,22 @@ class LocalEnergyEngine:
         est.k_total = int(st[3])
         return est
 
+    def set_code_override(self, codes) -> None:
+        """Test hook (include/vqnqs_b200_debug.h): force the VQ code of every
+        active location to codes[i, layer, row, position] (int16, rows in
+        bond order, -1 keeps the computed code) for calls on batches of
+        exactly len(codes) samples, so values after a flagged near-tie can be
+        compared with the reference's; None clears."""
+        f = N.lib().vqnqs_debug_set_code_override
+        f.restype = C.c_int
+        f.argtypes = [C.c_void_p, C.POINTER(C.c_int16), C.c_int64]
+        if codes is None:
+            N.check(f(self._h, None, 0))
+            return
+        c = np.ascontiguousarray(codes, np.int16)
+        self._override_keep = c
+        N.check(f(self._h, c.ctypes.data_as(C.POINTER(C.c_int16)), int(c.shape[0])))
+
     def set_micro_batch(self, samples: int) -> None:
         """Samples per micro-batch (0 = sized from the working-set budget)."""
         N.check(N.lib().vqnqs_gpu_set_micro_batch(self._h, int(samples)))

@@ -10,6 +10,7 @@
 
 #include "comm.h"
 #include "engine.h"
+#include "vqnqs_b200_debug.h"
 
 struct vqnqs_handle {
   vqb::Engine* eng;
@@ -166,6 +167,13 @@ int vqnqs_gpu_set_micro_batch(vqnqs_handle* h, int samples) {
     if (!h) throw vqb::UsageError("null handle");
     if (samples < 0) throw vqb::ConfigError("micro-batch size must be >= 0");
     h->eng->set_micro_batch(samples);
+  });
+}
+
+int vqnqs_debug_set_code_override(vqnqs_handle* h, const int16_t* codes, int64_t n_samples) {
+  return guarded([&] {
+    if (!h) throw vqb::UsageError("null handle");
+    h->eng->set_code_override(codes, n_samples);
   });
 }
 

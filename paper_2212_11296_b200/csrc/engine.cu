@@ -415,6 +415,21 @@ class EngineImpl {
 
   bool dense = false;  // no-reuse regime
   int fixed_chunk = 0;  // set_micro_batch: fixed samples per micro-batch (0 = auto)
+  // test hook: forced VQ codes [n][L][R1][T] (-1 = keep), see set_code_override
+  DBuf<int16_t> ovr_;
+  int64_t ovr_n_ = 0, chunk_s0_ = 0;
+  void set_code_override(const int16_t* host, int64_t n) {
+    CK(cudaSetDevice(dev));
+    if (!host || n <= 0) {
+      ovr_n_ = 0;
+      return;
+    }
+    if (H != 1) throw CapabilityError("code override supports vq_heads = 1 only");
+    const size_t cnt = size_t(n) * L * (nb + 1) * T;
+    ovr_.ensure(cnt);
+    CK(cudaMemcpy(ovr_.p, host, cnt * sizeof(int16_t), cudaMemcpyHostToDevice));
+    ovr_n_ = n;
+  }
   void set_micro_batch(int samples) {
     fixed_chunk = samples;
     size_chunks();
@@ -643,6 +658,11 @@ class EngineImpl {
           }
           vq_simt(tot + 0, M, att_.p, B.cb32, code_.p, st);
         }
+        if (ovr_n_ > 0) {  // test hook: the reference's codes at every location
+          k_code_override<<<sms * 4, 256, 0, st>>>(tot + 0, lrow_.p, lpos_.p, R1, T, L, b,
+                                                   chunk_s0_, ovr_.p, code_.p);
+          ++launches;
+        }
         CK(cudaEventRecord(lev[3 * b + 1], st));
         if (tap_codes) {
           std::vector<int32_t> hc(size_t(M) * H);
@@ -744,7 +764,8 @@ class EngineImpl {
       lp_rows_.ensure(R);
       lp_rows = lp_rows_.p;
     }
-    k_eloc<<<(S * 32 + 127) / 128, 128, 0, st>>>(S, R1, T, g, V, marshall ? -0.5 : 0.5, K_.p,
+    smem_optin(reinterpret_cast<const void*>(k_eloc), size_t(R1) * sizeof(double));
+    k_eloc<<<S, ELOC_THREADS, size_t(R1) * sizeof(double), st>>>(S, R1, T, g, V, marshall ? -0.5 : 0.5, K_.p,
                                                  diag_.p, row_bond_.p, row_t1_.p, row_aoff_.p,
                                                  act_off_.p, tok0_.p, d_bonds, Icur,
                                                  Uoff_.p + int64_t(L) * S, lpV_.p, d_e, d_logpsi,
@@ -813,8 +834,12 @@ class EngineImpl {
         if (!e) CK(cudaEventCreate(&e));
     }
     int64_t tap_code_pos = 0, tap_lp_pos = 0;
+    if (ovr_n_ > 0 && ovr_n_ != B)
+      throw UsageError("code override set for " + std::to_string(ovr_n_) +
+                       " samples, batch has " + std::to_string(B));
     for (int64_t s0 = 0; s0 < B; s0 += S_max) {
       const int S = int(std::min<int64_t>(S_max, B - s0));
+      chunk_s0_ = s0;
       std::vector<int32_t> hK, hU;
       std::vector<int32_t> tcodes;
       std::vector<int64_t> tact, taoff;
@@ -1167,6 +1192,7 @@ Engine::Engine(const vqnqs_model_desc& d, const double* const* params, int n_par
 Engine::~Engine() { delete p_; }
 void Engine::set_reuse(bool reuse) { p_->set_reuse(reuse); }
 void Engine::set_micro_batch(int samples) { p_->set_micro_batch(samples); }
+void Engine::set_code_override(const int16_t* codes, int64_t n) { p_->set_code_override(codes, n); }
 void Engine::fill_stats_device(const double* d_e, int64_t B, Comm* comm, void* stream,
                                double* stats) {
   p_->fill_stats_device(d_e, B, comm, stream ? static_cast<cudaStream_t>(stream) : p_->own,

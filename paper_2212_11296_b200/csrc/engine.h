@@ -89,6 +89,12 @@ class Engine {
   void set_reuse(bool reuse);
   // samples per micro-batch; 0 = sized from the working-set budget
   void set_micro_batch(int samples);
+  // Test hook: force the VQ code of every location to the given one
+  // (codes [n][L][nb + 1][T] int16 over rows in bond order, -1 = keep the
+  // computed code), for the next calls on batches of exactly n samples, so
+  // that values after a flagged near-tie can be compared with the
+  // reference's; null clears. vq_heads = 1 only.
+  void set_code_override(const int16_t* codes, int64_t n);
 
   struct Taps {
     int32_t* K = nullptr;       // [B]

@@ -600,15 +600,29 @@ __global__ void k_embed(int d, int R1, int T, int g, int V, const int32_t* __res
                         const int32_t* __restrict__ row_bond, const int32_t* __restrict__ bonds,
                         const float* __restrict__ tok_embed, const float* __restrict__ pos_embed,
                         float* __restrict__ x) {
+  // one warp per unique input row: its (position, token) once, then the row
+  // written as float4 (d % 4 == 0)
   const int s = blockIdx.x;
   const int U = Ucnt[s];
-  const int64_t base = act_off[s];
-  for (int64_t idx = threadIdx.x; idx < (int64_t)U * d; idx += blockDim.x) {
-    const int uid = int(idx / d), c = int(idx % d);
+  const int64_t base = act_off[s], uo = Uoff[s];
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int d4 = d >> 2;
+  for (int uid = threadIdx.x >> 5; uid < U; uid += nw) {
     const int64_t loc = base + rep_of[base + uid];
     const int r = lrow[loc], p = lpos[loc];
     const int tok = p == 0 ? V : row_token(tok0 + (int64_t)s * T, bonds, row_bond[r], g, p - 1);
-    x[(Uoff[s] + uid) * d + c] = tok_embed[(int64_t)tok * d + c] + pos_embed[(int64_t)p * d + c];
+    if ((d & 3) == 0) {
+      const float4* te = reinterpret_cast<const float4*>(tok_embed + (int64_t)tok * d);
+      const float4* pe = reinterpret_cast<const float4*>(pos_embed + (int64_t)p * d);
+      float4* xr = reinterpret_cast<float4*>(x + (uo + uid) * d);
+      for (int c = lane; c < d4; c += 32) {
+        const float4 a = te[c], b = pe[c];
+        xr[c] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+      }
+    } else {
+      for (int c = lane; c < d; c += 32)
+        x[(uo + uid) * d + c] = tok_embed[(int64_t)tok * d + c] + pos_embed[(int64_t)p * d + c];
+    }
   }
 }
 
@@ -623,18 +637,30 @@ __global__ void k_layernorm(const int64_t* __restrict__ Mp, int d, const float* 
   const int64_t M = *Mp;
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
-  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
-    const float* xr = x + r * d;
-    if (d <= 32 * LN_REG) {
-      // the row read once into registers (element lane + 32 k); same sums
+  const int64_t r0 = blockIdx.x * wpb + (threadIdx.x >> 5), rstep = (int64_t)gridDim.x * wpb;
+  if (d <= 32 * LN_REG) {
+    // rows read once into registers (element lane + 32 k), the warp's next
+    // row loaded before this row's reductions; same sums
+    float nx[LN_REG];
+#pragma unroll
+    for (int k = 0; k < LN_REG; ++k) {
+      const int c = lane + 32 * k;
+      nx[k] = (r0 < M && c < d) ? x[r0 * d + c] : 0.f;
+    }
+    for (int64_t r = r0; r < M; r += rstep) {
       float xv[LN_REG];
-      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k) xv[k] = nx[k];
+      const int64_t rn = r + rstep;
 #pragma unroll
       for (int k = 0; k < LN_REG; ++k) {
         const int c = lane + 32 * k;
-        xv[k] = c < d ? xr[c] : 0.f;
-        if (c < d) s += xv[k];
+        nx[k] = (rn < M && c < d) ? x[rn * d + c] : 0.f;
       }
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k)
+        if (lane + 32 * k < d) s += xv[k];
       const double mean = warp_sum(s) / d;
       double v = 0.0;
 #pragma unroll
@@ -650,8 +676,11 @@ __global__ void k_layernorm(const int64_t* __restrict__ Mp, int d, const float* 
         const int c = lane + 32 * k;
         if (c < d) out[r * d + c] = from_f<TA>((float)((xv[k] - mean) * rstd * gam[c] + bet[c]));
       }
-      continue;
     }
+    return;
+  }
+  for (int64_t r = r0; r < M; r += rstep) {
+    const float* xr = x + r * d;
     double s = 0.0;
     for (int c = lane; c < d; c += 32) s += xr[c];
     const double mean = warp_sum(s) / d;
@@ -682,7 +711,57 @@ __global__ void k_cont_ln(const int64_t* __restrict__ Mp, int d, int H, int Q,
   const int64_t M = *Mp;
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
-  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
+  const int64_t r0 = blockIdx.x * wpb + (threadIdx.x >> 5), rstep = (int64_t)gridDim.x * wpb;
+  if (H == 1 && d <= 32 * LN_REG) {
+    // y = x[g_res] + P[g_code] in registers between the passes, the warp's
+    // next row gathered before this row's reductions; same sums
+    float nxv[LN_REG], npv[LN_REG];
+    auto gather = [&](int64_t r, float* xv, float* pv) {
+      const bool ok = r < M;
+      const float* xr = x + (ok ? g_res[r] : 0) * d;
+      const float* pr = pwo + (int64_t)(ok ? g_code[r] : 0) * d;
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k) {
+        const int c = lane + 32 * k;
+        xv[k] = (ok && c < d) ? xr[c] : 0.f;
+        pv[k] = (ok && c < d) ? pr[c] : 0.f;
+      }
+    };
+    gather(r0, nxv, npv);
+    for (int64_t r = r0; r < M; r += rstep) {
+      float yv[LN_REG];
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k) yv[k] = nxv[k] + npv[k];
+      gather(r + rstep, nxv, npv);
+      float* yr = y + r * d;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k) {
+        const int c = lane + 32 * k;
+        if (c < d) {
+          yr[c] = yv[k];
+          s += yv[k];
+        }
+      }
+      const double mean = warp_sum(s) / d;
+      double q = 0.0;
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k)
+        if (lane + 32 * k < d) {
+          const double t = yv[k] - mean;
+          q += t * t;
+        }
+      const double var = warp_sum(q) / d;
+      const double rstd = 1.0 / sqrt(var + 1e-5);
+#pragma unroll
+      for (int k = 0; k < LN_REG; ++k) {
+        const int c = lane + 32 * k;
+        if (c < d) out[r * d + c] = from_f<TA>((float)((yv[k] - mean) * rstd * gam[c] + bet[c]));
+      }
+    }
+    return;
+  }
+  for (int64_t r = r0; r < M; r += rstep) {
     const float* xr = x + g_res[r] * d;
     const float* pr = pwo + (int64_t)g_code[r * H] * d;
     float* yr = y + r * d;
@@ -707,37 +786,6 @@ __global__ void k_cont_ln(const int64_t* __restrict__ Mp, int d, int H, int Q,
       const double rstd = 1.0 / sqrt(var + 1e-5);
       for (int c = lane; c < d; c += 32)
         out[r * d + c] = from_f<TA>((float)((yr[c] - mean) * rstd * gam[c] + bet[c]));
-      continue;
-    }
-    if (d <= 32 * LN_REG) {
-      // y kept in registers between the passes; same sums
-      float yv[LN_REG];
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < LN_REG; ++k) {
-        const int c = lane + 32 * k;
-        yv[k] = 0.f;
-        if (c < d) {
-          yv[k] = xr[c] + pr[c];
-          yr[c] = yv[k];
-          s += yv[k];
-        }
-      }
-      const double mean = warp_sum(s) / d;
-      double q = 0.0;
-#pragma unroll
-      for (int k = 0; k < LN_REG; ++k)
-        if (lane + 32 * k < d) {
-          const double t = yv[k] - mean;
-          q += t * t;
-        }
-      const double var = warp_sum(q) / d;
-      const double rstd = 1.0 / sqrt(var + 1e-5);
-#pragma unroll
-      for (int k = 0; k < LN_REG; ++k) {
-        const int c = lane + 32 * k;
-        if (c < d) out[r * d + c] = from_f<TA>((float)((yv[k] - mean) * rstd * gam[c] + bet[c]));
-      }
       continue;
     }
     double s = 0.0;
@@ -839,6 +887,22 @@ __global__ void k_join_split(const int64_t* __restrict__ Mp, int d, const bf16* 
 // The H codes of a location as one exact key: code_h << (h * qbits), either
 // as 32 bits (key32, the MODE 1 code operand directly) or 64 bits (tup, to be
 // numbered by k_dedup<2> first).
+// Test hook (Engine::set_code_override): code of active location loc of
+// layer b := ovr[((s0 + s) L + b) R1 + k][p] unless that entry is -1.
+__global__ void k_code_override(const int64_t* __restrict__ Mp, const int32_t* __restrict__ lrow,
+                                const int16_t* __restrict__ lpos, int R1, int T, int L, int b,
+                                int64_t s0, const int16_t* __restrict__ ovr,
+                                int32_t* __restrict__ code) {
+  const int64_t M = *Mp;
+  for (int64_t loc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; loc < M;
+       loc += (int64_t)gridDim.x * blockDim.x) {
+    const int r = lrow[loc];
+    const int s = r / R1, k = r - s * R1;
+    const int16_t v = ovr[(((s0 + s) * L + b) * R1 + k) * T + lpos[loc]];
+    if (v >= 0) code[loc] = v;
+  }
+}
+
 __global__ void k_pack_codes(const int64_t* __restrict__ Mp, int H, int qbits,
                              const int32_t* __restrict__ code, unsigned long long* __restrict__ tup,
                              int32_t* __restrict__ key32) {
@@ -865,10 +929,11 @@ __global__ void k_head(const int64_t* __restrict__ Mp, int d, int V, int lastV, 
   double logit[16];
   for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
     for (int c = 0; c < V; ++c) {
-      float acc = 0.f;
-      for (int e = lane; e < d; e += 32) acc += to_f<TA>(h[r * d + e]) * to_f<TA>(W[(int64_t)e * V + c]);
+      double acc = 0.0;  // products of fp32 / bf16 operands are exact in double
+      for (int e = lane; e < d; e += 32)
+        acc += (double)to_f<TA>(h[r * d + e]) * (double)to_f<TA>(W[(int64_t)e * V + c]);
       acc = warp_sum(acc);
-      logit[c] = (double)(acc + b[c]);
+      logit[c] = acc + (double)b[c];
       if (lastV < V && c >= lastV && upos[r] == T - 1) logit[c] = -1e30;
     }
     double mx = logit[0];
@@ -889,43 +954,61 @@ __global__ void k_head(const int64_t* __restrict__ Mp, int d, int V, int lastV, 
 // 410-417). lp_k - lp_0 is accumulated only over positions p >= t1_k, where
 // row k's target token or hidden state can differ from the base row's; the
 // shared prefix cancels exactly. E = diag + sum_{k>=1} c * exp(0.5 (lp_k - lp_0)).
-__global__ void k_eloc(int S, int R1, int T, int g, int V, double coeff,
-                       const int32_t* __restrict__ K, const double* __restrict__ diag,
-                       const int32_t* __restrict__ row_bond, const int32_t* __restrict__ row_t1,
-                       const int64_t* __restrict__ row_aoff, const int64_t* __restrict__ act_off,
-                       const int32_t* __restrict__ tok0, const int32_t* __restrict__ bonds,
-                       const int32_t* __restrict__ I_L, const int64_t* __restrict__ Uoff_L,
-                       const double* __restrict__ lpV, double* __restrict__ e_out,
-                       double* __restrict__ logpsi, double* __restrict__ lp_rows) {
-  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (s >= S) return;
+// One CTA (256 threads) per sample: warp w takes rows k = 1 + w, 1 + w + 8,
+// ..., its lanes the positions of a row (sum in a fixed shuffle tree); the
+// row terms land in shared memory and warp 0 adds them in row order, so a
+// sample's energy does not depend on the micro-batch it ran in.
+constexpr int ELOC_THREADS = 256;
+__global__ void __launch_bounds__(ELOC_THREADS) k_eloc(
+    int S, int R1, int T, int g, int V, double coeff, const int32_t* __restrict__ K,
+    const double* __restrict__ diag, const int32_t* __restrict__ row_bond,
+    const int32_t* __restrict__ row_t1, const int64_t* __restrict__ row_aoff,
+    const int64_t* __restrict__ act_off, const int32_t* __restrict__ tok0,
+    const int32_t* __restrict__ bonds, const int32_t* __restrict__ I_L,
+    const int64_t* __restrict__ Uoff_L, const double* __restrict__ lpV,
+    double* __restrict__ e_out, double* __restrict__ logpsi, double* __restrict__ lp_rows) {
+  extern __shared__ double el_term[];  // [R1]
+  __shared__ double lp0_s;
+  const int s = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int32_t* t0 = tok0 + (int64_t)s * T;
   const int64_t base = act_off[s];
   const int64_t uo = Uoff_L[s];
-  double lp0 = 0.0;
-  for (int p = lane; p < T; p += 32) lp0 += lpV[(uo + I_L[base + p]) * V + t0[p]];
-  lp0 = warp_sum(lp0);
+  if (w == 0) {
+    double lp0 = 0.0;
+    for (int p = lane; p < T; p += 32) lp0 += lpV[(uo + I_L[base + p]) * V + t0[p]];
+    lp0 = warp_sum(lp0);
+    if (lane == 0) lp0_s = lp0;
+  }
   const int Ks = K[s];
-  double acc = 0.0;
-  for (int k = 1 + lane; k < Ks; k += 32) {
+  __syncthreads();
+  const double lp0 = lp0_s;
+  for (int k = 1 + w; k < Ks; k += nw) {
     const int64_t r = (int64_t)s * R1 + k;
     const int bond = row_bond[r], t1 = row_t1[r], a = t1 + 1;
     const int64_t rloc = base + row_aoff[r];
     double diff = 0.0;
-    for (int p = max(t1, 0); p < T; ++p) {  // t1 = -1 in the no-reuse regime
+    for (int p = max(t1, 0) + lane; p < T; p += 32) {  // t1 = -1 in the no-reuse regime
       const int64_t u0 = uo + I_L[base + p];
       const int64_t uk = p < a ? u0 : uo + I_L[rloc + (p - a)];
       diff += lpV[uk * V + row_token(t0, bonds, bond, g, p)] - lpV[u0 * V + t0[p]];
     }
-    acc += coeff * exp(0.5 * diff);
-    if (lp_rows) lp_rows[r] = lp0 + diff;
+    diff = warp_sum(diff);
+    if (lane == 0) {
+      el_term[k] = coeff * exp(0.5 * diff);
+      if (lp_rows) lp_rows[r] = lp0 + diff;
+    }
   }
-  acc = warp_sum(acc);
-  if (lane == 0) {
-    e_out[s] = diag[s] + acc;
-    logpsi[s] = 0.5 * lp0;
-    if (lp_rows) lp_rows[(int64_t)s * R1] = lp0;
+  __syncthreads();
+  if (w == 0) {
+    double acc = 0.0;
+    for (int k = 1 + lane; k < Ks; k += 32) acc += el_term[k];
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      e_out[s] = diag[s] + acc;
+      logpsi[s] = 0.5 * lp0;
+      if (lp_rows) lp_rows[(int64_t)s * R1] = lp0;
+    }
   }
 }
 

@@ -31,12 +31,20 @@ __global__ void __launch_bounds__(256) k_gemm_simt(
   for (int64_t tile = blockIdx.x; tile < tilesM * tilesN; tile += gridDim.x) {
     const int64_t m0 = (tile / tilesN) * BM;
     const int n0 = int(tile % tilesN) * BN;
-    float acc[4][4];
+    // fp32 products summed per BK block, the block sums added in double:
+    // the K-length accumulation error stays at a few fp32 ulps instead of
+    // growing with sqrt(K) (K = 4d = 3072 at c5)
+    double dacc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+      for (int j = 0; j < 4; ++j) dacc[i][j] = 0.0;
     for (int k0 = 0; k0 < K; k0 += BK) {
+      float acc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int e = tid + q * 256;
@@ -66,6 +74,10 @@ __global__ void __launch_bounds__(256) k_gemm_simt(
           for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
       }
       __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dacc[i][j] += acc[i][j];
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -75,7 +87,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(
       for (int j = 0; j < 4; ++j) {
         const int n = n0 + tx * 4 + j;
         if (n >= N) continue;
-        const float v = acc[i][j] + bias[n];
+        const float v = (float)(dacc[i][j] + (double)bias[n]);
         if (EPI == EPI_STORE) {
           static_cast<TA*>(out)[m * ldo + n] = from_f<TA>(v);
         } else if (EPI == EPI_GELU) {

@@ -47,6 +47,17 @@ BF16_ELOC_RTOL = 2e-3
 BF16_LOGPSI_TOL_DEEP = 1e-2
 # c5 (12 blocks, d=768, 1024 codes): measured 4.2e-2
 BF16_LOGPSI_TOL_C5 = 2.5e-2
+# connected rows' log-probs (they enter E_loc only through exp((lp_k -
+# lp_0) / 2), which the E_loc tolerance bounds): the largest clean-row drift
+# over the reference fixtures' rows is 2.09e-2 at c4 (2136 rows) and 5.8e-2
+# at c5 (1188 rows) against the bf16 emulation
+BF16_LP_ROW_TOL_DEEP = 3e-2
+BF16_LP_ROW_TOL_C5 = 8e-2
+# E_loc sums K ~ 260 (c4) / 150 (c5) such ratios: with the reference's codes
+# forced at every location, the largest relative E_loc deviation from the
+# bf16 emulation is 1.9e-3 at c4 and 9.2e-3 at c5 (8 samples each)
+BF16_ELOC_RTOL_DEEP = 4e-3
+BF16_ELOC_RTOL_C5 = 1.5e-2
 
 
 @dataclass
@@ -54,6 +65,7 @@ class ParityReport:
     window: float = GAP_FLAG
     logpsi_tol: float = LOGPSI_TOL
     eloc_rtol: float = ELOC_RTOL
+    lp_row_tol: float = 0.0  # per-row log-prob tolerance; 0 = 2 logpsi_tol
     samples: int = 0
     clean_samples: int = 0
     rows: int = 0
@@ -143,6 +155,17 @@ class FixtureTaps:
         self.lp = np.asarray(lp, np.float64)
 
 
+def override_codes(z, taps, L, R1, T):
+    """The fixture's reference codes as the engine's code override
+    (Engine::set_code_override): int16 [n, L, R1, T], rows in bond order,
+    -1 past a sample's K rows."""
+    n = len(taps)
+    out = np.full((n, L, R1, T), -1, np.int16)
+    for i, t in enumerate(taps):
+        out[i, :, :t.K, :] = t.codes[..., 0].reshape(L, t.K, T)
+    return out
+
+
 def load_fixture(path):
     """(dict of arrays, [FixtureTaps per sample]) of a parity_<case>.npz."""
     z = np.load(path)
@@ -193,7 +216,7 @@ def compare(rep: ParityReport, taps, ref_e, ref_lpsi, gpu_codes, gpu_U, gpu_e, g
     if clean.any():
         dlp = np.abs(np.asarray(gpu_lp_rows)[clean] - taps.lp[clean])
         rep.max_dlp = max(rep.max_dlp, float(dlp.max()))
-        rep.lp_fail += int((dlp > 2 * rep.logpsi_tol).sum())
+        rep.lp_fail += int((dlp > (rep.lp_row_tol or 2 * rep.logpsi_tol)).sum())
     if clean[0]:
         rep.logpsi_checked += 1
         dl = abs(float(ref_lpsi) - float(gpu_lpsi))
