@@ -137,7 +137,7 @@ class EngineImpl {
   int qbits = 1;            // bits per VQ code in the packed tuple key
   bool tuple_pass = false;  // H codes exceed 32 bits: number tuples first
   bool use_tc_gemm = false;  // tcgen05 per-location GEMMs (bf16)
-  bool use_tc_vq = false;    // tcgen05 certified-argmin VQ (bf16)
+  bool use_tc_vq = false;    // tcgen05 certified-argmin VQ (both precisions)
   bool use_tc_attn = false;  // tcgen05 gathered attention (bf16)
   unsigned long long* d_rescored = nullptr;
   std::vector<void*> allocs;
@@ -242,7 +242,7 @@ class EngineImpl {
     lastV = (N % g == 0) ? V : 1 << (N % g);
     if (T > 1024 || dh > 256) throw CapabilityError("GPU path: T <= 1024, head dim <= 256");
     use_tc_gemm = tc_gemm_ok(prec, d, d) && tc_gemm_ok(prec, 4 * d, d);
-    use_tc_vq = H == 1 && c.vq_enabled && tc_vq_ok(prec, d, Q);
+    use_tc_vq = H == 1 && c.vq_enabled && tc_vq_ok(d, Q);
     // dedup key of a location after a VQ: (residual row, code tuple); H codes
     // of ceil(log2 Q) bits pack into the key's low 32 bits when they fit,
     // otherwise the tuple is first numbered by its own exact-key pass
@@ -311,7 +311,11 @@ class EngineImpl {
         B.werr = float(pc.werr);
         if (prec == VQNQS_PREC_BF16) B.cbA = upload(pc.bf);
         else B.cbA = upload_op(std::vector<double>(cb, cb + (size_t)Q * d));
-        if (use_tc_vq) B.tmB = make_tmap_bf16(B.cbA, uint64_t(Q), uint64_t(d), 256);
+        // the certified-argmin kernel's bf16 codebook operand (in fp32 mode the
+        // codebook's bf16 rounding error enters its bound, werr)
+        if (use_tc_vq)
+          B.tmB = make_tmap_bf16(prec == VQNQS_PREC_BF16 ? B.cbA : upload(pc.bf), uint64_t(Q),
+                                 uint64_t(d), 256);
       }
       if (B.has_ffn) {
         B.ln2_g = upload_f(ln2g, d);

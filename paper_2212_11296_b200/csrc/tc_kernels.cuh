@@ -19,9 +19,11 @@ namespace vqb {
 inline bool tc_gemm_ok(int prec, int N, int K) {
   return prec == 1 && K % 64 == 0 && N % 64 == 0;
 }
-// ... and the VQ kernel keeps all Q code norms resident in shared memory.
-inline bool tc_vq_ok(int prec, int d, int Q) {
-  return prec == 1 && d % 64 == 0 && Q % 256 == 0 && tcv_smem_bytes(Q) <= smem_optin_limit();
+// The VQ kernel keeps all Q code norms resident in shared memory.
+// The certified argmin is exact in both precisions (ties to the lowest
+// index, ambiguous rows re-scored in double), so the fp32 engine uses it too.
+inline bool tc_vq_ok(int d, int Q) {
+  return d % 64 == 0 && Q % 256 == 0 && tcv_smem_bytes(Q) <= smem_optin_limit();
 }
 
 template <int BN, int EPI>
