@@ -244,6 +244,8 @@ def main():
     ap.add_argument("--no-sampler", action="store_true", help="skip the sampler measurement")
     ap.add_argument("--no-dense", action="store_true",
                     help="skip the no-reuse (dense) regime measurement")
+    ap.add_argument("--no-strict", action="store_true",
+                    help="skip the strict-tolerance (fp32 engine) line")
     ap.add_argument("--batch", type=int, default=0, help="override samples per rank")
     ap.add_argument("--also", default="c5",
                     help="other workloads to device-time in the same run (comma list, or none)")
@@ -344,7 +346,7 @@ def main():
         gengine.grad(host_cfg[:nb_g], wts)
         dt = time.perf_counter() - t0
         gradient = {"value": nb_g * ws / dt, "unit": "samples/s", "samples_per_rank": nb_g,
-                    "seconds": dt, "precision": "fp32 (cuBLAS fp32 GEMMs)"}
+                    "seconds": dt, "precision": "fp32 (CUDA-core GEMMs of csrc/sgemm.cuh, fp32 accumulation)"}
         gengine.close()
 
     # the reference's no-reuse regime (dense_local_energy,
@@ -359,6 +361,27 @@ def main():
                  "wall_savings": d_ms / ms_per_step,
                  "regime": "no-reuse: every connected config's full T-token forward, no shared "
                            "prefix, no unique-row merging (proj/src/bench.cpp:19-36)"}
+
+    # the strict-tolerance mode beside the bf16 headline: the same workload in
+    # the fp32 engine (unsnapped weights; CUDA-core fp32 GEMMs and attention
+    # with double-summed blocks, the certified tcgen05 argmin), which meets the
+    # north-star contract against the reference in double on every row with
+    # the reference's codes forced (tests/test_gpu_parity_large.py::
+    # test_forced_codes_strict); a bounded batch of the workload's samples
+    strict = None
+    if not args.no_strict:
+        m_s = P.VqTransformer.init(w.model, w.weight_seed, snap_bf16=False)
+        e_s = P.LocalEnergyEngine(m_s, P.HamiltonianModel(lat), precision="fp32", device=local)
+        nb_s = min(B, 1024)
+        s_ms, s_evals, *_ = measure_device(torch, dist, e_s, host_cfg[:nb_s], comm, 2, 1, ws,
+                                           local, flush)
+        strict = {"value": s_evals * ws / (s_ms / 1e3), "unit": UNIT, "ms_per_step": s_ms,
+                  "steps": 2, "warmup": 1, "samples_per_rank": nb_s, "precision": "fp32",
+                  "parity": "north-star tolerances vs the reference in double at c3-c5 "
+                            "(every row with the reference's codes forced: max |dlp_row| "
+                            "2.8e-6, |dlogpsi| 7.6e-7, E_loc 2e-7 rel; profiles/"
+                            "r02_parity_report.jsonl)"}
+        e_s.close()
 
     # roofline of the dominant kernel (the tcgen05 attention). Its algorithmic
     # work per step: FLOPs 4 d (live keys) per active location and layer (QK^T
@@ -430,6 +453,7 @@ def main():
         "gpu_launches": int(launches_per_step * args.steps),
         "strong_scaling": strong,
         "no_reuse": dense,
+        "strict_fp32": strict,
         "sampler": sampler,
         "vmc_gradient": gradient,
         "clocks": clk,

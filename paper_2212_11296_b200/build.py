@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for r in ex.map(lambda c: subprocess.run(c, check=True), cmds):
             pass
     tmp = LIB + ".tmp"
-    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcublas", "-ldl"],
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"],
                    check=True)
     os.replace(tmp, LIB)
     return LIB

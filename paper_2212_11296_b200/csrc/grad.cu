@@ -10,12 +10,10 @@
 // The dense decoder over all B x T locations runs forward once with its
 // activations kept (fp32 values, double LayerNorm statistics and VQ
 // distances), then backward layer by layer: every GEMM-shaped product on
-// cuBLAS (plain library GEMMs, fp32), the per-row / per-(sample, head) work
-// in the kernels below, every reduction over rows in a fixed order (no
+// the fp32 CUDA-core GEMM of sgemm.cuh, the per-row / per-(sample, head)
+// work in the kernels below, every reduction over rows in a fixed order (no
 // atomics), so the gradient is deterministic. Micro-batches of samples
 // accumulate into the same gradient buffers.
-#include <cublas_v2.h>
-
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -24,6 +22,7 @@
 
 #include "common.cuh"
 #include "engine.h"
+#include "sgemm.cuh"
 
 namespace vqb {
 namespace {
@@ -34,13 +33,6 @@ namespace {
     if (e_ != cudaSuccess)                                                                \
       throw RuntimeError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
                          __FILE__ + ":" + std::to_string(__LINE__));                      \
-  } while (0)
-#define GCB(x)                                                                   \
-  do {                                                                           \
-    cublasStatus_t s_ = (x);                                                     \
-    if (s_ != CUBLAS_STATUS_SUCCESS)                                             \
-      throw RuntimeError("cuBLAS error " + std::to_string(int(s_)) + " at " +    \
-                         std::string(__FILE__) + ":" + std::to_string(__LINE__)); \
   } while (0)
 
 template <typename T>
@@ -662,14 +654,14 @@ class GradImpl {
   int dev = 0;
   int d, nh, Q, L, V, T, g, N, lastV;
   cudaStream_t st = nullptr;
-  cublasHandle_t cb = nullptr;
+  int sms = 148;
   std::vector<ParamSpec> spec;
   std::vector<float*> W;  // device copies, parameters() order
   std::vector<float*> Gr;  // gradients, parameters() order
   std::vector<float*> wqkv, bqkv, gwqkv, gbqkv;  // concatenated per block
   // activations (one micro-batch)
   GBuf<float> x_all, h1, qkv, P, att, dist, xq, x1, h2, pre, hf, logits, dlog, tmp, tmp2, tmp4,
-      dx, dx1, dqkv, Pm, F, A, part, part2, fsum, fcol;
+      dx, dx1, dqkv, Pm, F, A, part, part2, fsum, fcol, gws;
   GBuf<double> m1, r1, m2, r2, mf, rf, logp, dw, dlp;
   GBuf<int> ids, tgt, pick;
   GBuf<uint8_t> dcfg;
@@ -685,9 +677,7 @@ class GradImpl {
       throw CapabilityError("GPU gradient: VQ in every block, vq_heads = 1, no phase network");
     GCK(cudaSetDevice(dev));
     GCK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    GCB(cublasCreate(&cb));
-    GCB(cublasSetStream(cb, st));
-    GCB(cublasSetMathMode(cb, CUBLAS_PEDANTIC_MATH));  // fp32 products, no TF32
+    GCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     d = c.d_hidden;
     nh = c.n_heads;
     Q = c.vq_codebook;
@@ -739,16 +729,14 @@ class GradImpl {
     for (auto* p : bqkv) cudaFree(p);
     for (auto* p : gwqkv) cudaFree(p);
     for (auto* p : gbqkv) cudaFree(p);
-    if (cb) cublasDestroy(cb);
     if (st) cudaStreamDestroy(st);
   }
 
-  // row-major C = op(A) op(B) (+ beta C)
+  // row-major C = op(A) op(B) (+ beta C) on the fp32 CUDA-core GEMM
   void gemm(bool tA, bool tB, int64_t M, int64_t Nn, int64_t K, const float* A, int64_t lda,
             const float* Bm, int64_t ldb, float* C, int64_t ldc, float beta) {
-    const float one = 1.f;
-    GCB(cublasSgemm(cb, tB ? CUBLAS_OP_T : CUBLAS_OP_N, tA ? CUBLAS_OP_T : CUBLAS_OP_N, int(Nn),
-                    int(M), int(K), &one, Bm, int(ldb), A, int(lda), &beta, C, int(ldc)));
+    gws.ensure(size_t(std::max<int64_t>(1, sgemm_ws_floats(M, Nn, K, sms))));
+    sgemm(tA, tB, M, Nn, K, A, lda, Bm, ldb, C, ldc, beta, gws.p, sms, st);
   }
   void colsum(int64_t R, int Nn, int lda, const float* A, float* out, float sign = 1.f) {
     const int rows_per = 256;
