@@ -156,13 +156,14 @@ class FixtureTaps:
 
 
 def override_codes(z, taps, L, R1, T):
-    """The fixture's reference codes as the engine's code override
-    (Engine::set_code_override): int16 [n, L, R1, T], rows in bond order,
-    -1 past a sample's K rows."""
+    """The reference's codes (fixture taps or live oracle taps) as the
+    engine's code override (Engine::set_code_override): int16 [n, L, R1, T],
+    rows in bond order, -1 past a sample's K rows. z is unused (kept for the
+    call sites that pass a fixture)."""
     n = len(taps)
     out = np.full((n, L, R1, T), -1, np.int16)
     for i, t in enumerate(taps):
-        out[i, :, :t.K, :] = t.codes[..., 0].reshape(L, t.K, T)
+        out[i, :, :t.K, :] = np.asarray(t.codes)[..., 0].reshape(L, t.K, T)
     return out
 
 

@@ -49,3 +49,40 @@ def test_dense_equals_compressed(name, n, ltol, etol):
     # and its ledger is the dense one (the reference's total_dense)
     assert led_d.total_dedup() == led_d.total_dense()
     assert led_c.total_dense() == led_d.total_dense()
+
+
+@pytest.mark.parametrize("name,n", [("c1_4x4", 16), ("c2_6x6", 8)])
+def test_dense_matches_oracle_dense_log_prob(port, name, n):
+    """The GPU's no-reuse regime row by row against the oracle's own dense
+    forward (dense_log_prob, proj/src/model.cpp:398-426): every connected
+    configuration's log P within 2e-5 and E_loc within 1e-4 relative of the
+    oracle's local energies. The oracle's VQ codes are forced at every
+    location (LocalEnergyEngine.set_code_override), so flagged near-ties
+    cannot make a row incomparable."""
+    from parity import override_codes
+
+    w, eng = _engine(name, "fp32")
+    lat = P.build_lattice("grid2d", (w.L, w.L), periodic=True)
+    port.set_bf16(False)
+    om = port.model(w.model, w.weight_seed)
+    oh = port.hamiltonian("grid_periodic", w.L, w.L)
+    S = P.zero_sz_samples(w.n_sites, 0, n, w.sample_seed)
+    taps = [om.taps(oh, s) for s in S]
+    m = w.model
+    eng.set_reuse(False)
+    eng.set_code_override(override_codes(None, taps, m.n_layers, lat.bonds.shape[0] + 1,
+                                         m.seq_len))
+    try:
+        e, lpsi = eng.local_energies(S)
+        K, U, _, lps = eng.taps(S)
+    finally:
+        eng.set_code_override(None)
+        eng.set_reuse(True)
+    ref_e, _, ref_lpsi, _ = om.local_energies(oh, S, workers=4)
+    for i, s in enumerate(S):
+        cf, _ = oh.connected_set(s)
+        ref_rows = om.dense_log_prob(cf)  # the reference's dense forward per configuration
+        assert int(K[i]) == cf.shape[0]
+        assert np.max(np.abs(np.asarray(lps[i]) - ref_rows)) < 2e-5
+        assert abs(lpsi[i] - 0.5 * ref_rows[0]) < 1e-5
+    assert np.max(np.abs(e.real - ref_e) / np.maximum(np.abs(ref_e), 1e-12)) < 1e-4
