@@ -928,12 +928,21 @@ __global__ void k_head(const int64_t* __restrict__ Mp, int d, int V, int lastV, 
   const int64_t wpb = blockDim.x >> 5;
   double logit[16];
   for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < M; r += (int64_t)gridDim.x * wpb) {
-    for (int c = 0; c < V; ++c) {
-      double acc = 0.0;  // products of fp32 / bf16 operands are exact in double
-      for (int e = lane; e < d; e += 32)
-        acc += (double)to_f<TA>(h[r * d + e]) * (double)to_f<TA>(W[(int64_t)e * V + c]);
-      acc = warp_sum(acc);
-      logit[c] = acc + (double)b[c];
+    // one pass over the row for all V logits; products of fp32 / bf16
+    // operands are exact in double
+    double acc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+    for (int e = lane; e < d; e += 32) {
+      const double he = (double)to_f<TA>(h[r * d + e]);
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < V) acc[c] += he * (double)to_f<TA>(W[(int64_t)e * V + c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      if (c >= V) break;
+      logit[c] = warp_sum(acc[c]) + (double)b[c];
       if (lastV < V && c >= lastV && upos[r] == T - 1) logit[c] = -1e30;
     }
     double mx = logit[0];
