@@ -79,3 +79,32 @@ def test_degenerate_batches(port, name):
     # an empty batch
     e0, l0 = eng.local_energies(S[:0], None)
     assert e0.shape == (0,) and l0.shape == (0,)
+
+
+def test_more_bonds_than_scratch_rows(port):
+    """A 24x24 periodic lattice has 1152 bonds, so a Néel configuration has
+    1153 connected rows: more rows than tokens (T = 288) and more than the
+    1025-row per-warp scratch of the first k_connected (sized since as
+    max(T, n_bonds + 1)). fp32 engine against the oracle, strict contract."""
+    L = 24
+    cfg = P.ModelConfig(n_sites=L * L, group_size=2, d_hidden=32, n_heads=4, n_blocks=1,
+                        trailing_half_block=False, vq_codebook=64, vq_init_scale=1.0 / 32)
+    model = P.VqTransformer.init(cfg, 0)
+    lat = P.build_lattice("grid2d", (L, L), periodic=True)
+    eng = P.LocalEnergyEngine(model, P.HamiltonianModel(lat), precision="fp32")
+    port.set_bf16(False)
+    om = port.model(cfg, 0)
+    oh = port.hamiltonian("grid_periodic", L, L)
+    x, y = np.meshgrid(np.arange(L), np.arange(L), indexing="xy")
+    neel = ((x + y) % 2).reshape(-1).astype(np.uint8)
+    S = np.stack([neel, 1 - neel, P.zero_sz_samples(L * L, 0, 1, 7)[0]])
+    ref_e, _, ref_lpsi, _ = om.local_energies(oh, S, workers=os.cpu_count() or 8)
+    e, lpsi = eng.local_energies(S, None)
+    K, U, codes, lps = eng.taps(S)
+    assert int(K[0]) == len(lat.bonds) + 1 == 1153
+    rep = ParityReport()
+    for i in range(len(S)):
+        compare(rep, om.taps(oh, S[i]), ref_e[i], ref_lpsi[i], codes[i], U[i], e[i].real,
+                lpsi[i], lps[i], cfg.seq_len)
+    print(f"\n[24x24 Néel] {rep.summary()}")
+    assert rep.ok(), rep.summary() + "\n" + "\n".join(rep.notes[:10])
