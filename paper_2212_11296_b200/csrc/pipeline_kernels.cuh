@@ -181,11 +181,15 @@ __global__ void k_connected(int S, int N, int g, int T, int nb, int dense,
   // Tiles of <= 128 active locations by a two-pointer sweep over the sorted
   // rows (the longest left first, then the next longest while they fit, then
   // the shortest while they fit): ~19% fewer attention tiles than a greedy
-  // sweep of the sorted order at c4, and a tile pairs long rows (short base
-  // prefix, long causal own range) with short ones (long prefix, short own
-  // range), which evens its row quadrants' work. The layout order is the tile
-  // order (k_build_tiles' greedy sweep reproduces these tiles); the base row
-  // (the longest) stays first, at the sample's layout offset 0.
+  // sweep of the sorted order at c4. Inside a tile the SHORT rows come first
+  // and the long ones last: a short row has many base keys and few own keys,
+  // a long row's causal own range grows with the tile row, so this order
+  // evens the live score chunks of the tile's four row quadrants (the
+  // attention softmax waits for the slowest quadrant; scripts/tile_sim.py:
+  // the maximum over quadrants drops 11% at c4, 18% at c5). The tile that
+  // holds the base row keeps it first: the base row stays at the sample's
+  // layout offset 0. Bit 30 of a row_perm entry marks the first row of a tile
+  // (k_build_tiles cuts there).
   if (lane == 0) {
     int* srt = sloc;  // rows sorted by t1, base row first
     int* ord = hist;  // layout order
@@ -193,26 +197,41 @@ __global__ void k_connected(int S, int N, int g, int T, int nb, int dense,
     srt[0] = 0;
     for (int i = 1; i < nrows; ++i) srt[i] = row_perm[pb + i];
     auto len = [&](int k) { return k == 0 ? T : T - (row_t1[pb + k] + 1); };
-    int i = 0, j = nrows - 1, o = 0;
-    int64_t off = 0;
-    auto put = [&](int k) {
-      ord[o++] = k;
-      row_aoff[pb + k] = off;
-      off += len(k);
+    auto rev = [&](int b, int e) {  // reverse ord[b, e)
+      for (--e; b < e; ++b, --e) {
+        const int t = ord[b];
+        ord[b] = ord[e];
+        ord[e] = t;
+      }
     };
+    int i = 0, j = nrows - 1, o = 0;
     while (i <= j) {
+      const int o0 = o;
       int c = len(srt[i]);
-      put(srt[i++]);
+      ord[o++] = srt[i++];
       while (i <= j && c + len(srt[i]) <= 128) {
         c += len(srt[i]);
-        put(srt[i++]);
+        ord[o++] = srt[i++];
       }
+      const int om = o;
       while (j >= i && c + len(srt[j]) <= 128) {
         c += len(srt[j]);
-        put(srt[j--]);
+        ord[o++] = srt[j--];
       }
+      if (o0 > 0) {  // [long..., short...] -> [short..., long...], each group's order kept
+        rev(o0, om);
+        rev(om, o);
+        rev(o0, o);
+      }
+      ord[o0] |= 1 << 30;
     }
-    for (int q = 0; q < nrows; ++q) row_perm[pb + q] = ord[q];
+    int64_t off = 0;
+    for (int q = 0; q < nrows; ++q) {
+      const int k = ord[q] & ~(1 << 30);
+      row_aoff[pb + k] = off;
+      off += len(k);
+      row_perm[pb + q] = ord[q];
+    }
   }
 }
 

@@ -49,8 +49,10 @@ struct AttnTile {
   int64_t loc0;  // first active location (global)
 };
 
-// Greedy packing of whole rows (consecutive in active-location order) into
-// tiles of <= 128 locations, one thread per sample, in two passes: pass 0
+// Packing of whole rows (consecutive in active-location order) into tiles of
+// <= 128 locations: a tile ends where k_connected marked the next row as a
+// tile start, or (unmarked orders: the no-reuse regime) where the next row
+// no longer fits. One thread per sample, in two passes: pass 0
 // counts each sample's tiles (tcnt), pass 1 writes them at the sample's
 // exclusive-scan offset (toff, k_scan) so a sample's tiles are contiguous in
 // the tile list. The persistent attention kernel deals tiles round-robin over
@@ -67,19 +69,23 @@ __global__ void k_build_tiles(int pass, int S, int R1, int T, const int32_t* __r
   if (s >= S) return;
   const int Ks = K[s];
   int cur = 0, nt = 0;
+  bool cut = false;
   int64_t start = act_off[s];
   const int64_t base = pass == 1 ? toff[s] : 0;
   for (int i = 0; i < Ks; ++i) {  // rows in active-layout order (k_connected)
-    const int k = row_perm[(int64_t)s * R1 + i];
+    const int kf = row_perm[(int64_t)s * R1 + i];  // bit 30: first row of a tile (k_connected)
+    const int k = kf & ~(1 << 30);
     const int n = k == 0 ? T : T - (row_t1[(int64_t)s * R1 + k] + 1);
+    cut |= kf != k;
     if (n <= 0) continue;
-    if (cur + n > 128) {
+    if (cur + n > 128 || (cut && cur > 0)) {
       if (pass == 1) tiles[base + nt] = AttnTile{s, cur, start};
       ++nt;
       start += cur;
       cur = 0;
     }
     cur += n;
+    cut = false;
   }
   if (cur > 0) {
     if (pass == 1) tiles[base + nt] = AttnTile{s, cur, start};
@@ -629,59 +635,89 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         ATR(0)
         // ---- the warp's live 16-column chunks (base chunks, then own chunks)
         // are dealt round-robin to the four warpgroups: slot i is chunk
-        // part + 4i. ONE TMEM pass loads them into registers.
+        // part + 4i, live slots are a prefix. Each chunk is processed on its
+        // own as soon as it is in registers -- mask, chunk max m_i,
+        // e = exp2((s - m_i) scale log2e), chunk sum -- while the next chunk's
+        // TMEM load is in flight, so the four warps of a sub-partition drift
+        // into different phases and the ALU-bound masking of one overlaps the
+        // MUFU-bound exponentials of another (with one max pass over all
+        // chunks first, the four ran both phases in lockstep). The per-chunk
+        // references are folded into the row's normaliser below, like the
+        // per-warp ones.
         float v[4][16];
-        bool sl[4], full[4];
-        uint32_t pcol[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          sl[i] = (sflags >> i) & 1u;
-          full[i] = (sflags >> (4 + i)) & 1u;
-          pcol[i] = sc_[i] >> 9;
-          if (sl[i]) tc::tmem_ld16(trow + (sc_[i] & 511u), v[i]);
-        }
+        float cm[4], cs[4];
+        const int nl = __popc(sflags & 15u);
+        if (nl > 0) tc::tmem_ld16(trow + (sc_[0] & 511u), v[0]);
         tc::tmem_wait_ld();
-        tc::fence_before();
-        arrive(s_free);  // the MMA warp may overwrite S with the next head's scores
-        ATR(1)
-        // ---- local max and sum of exp2((s - m_part) * scale * log2e)
-        float mp = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (!sl[i]) continue;
-          if (full[i]) {
-#pragma unroll
-            for (int q = 0; q < 16; ++q) mp = fmaxf(mp, v[i][q]);
-          } else {
-            const uint32_t m16 = mk_[i >> 1] >> (16 * (i & 1));
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              v[i][q] = (m16 >> q) & 1u ? v[i][q] : -INFINITY;
-              mp = fmaxf(mp, v[i][q]);
-            }
-          }
+        if (nl == 0) {
+          tc::fence_before();
+          arrive(s_free);
         }
-        const float mref = mp == -INFINITY ? 0.f : mp * sl2;
-        float2 sp2 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          if (!sl[i]) continue;
+          cm[i] = -INFINITY;
+          cs[i] = 0.f;
+          if (i < nl) {
+            if (i + 1 < nl) {
+              if (i < 3) tc::tmem_ld16(trow + (sc_[i < 3 ? i + 1 : 3] & 511u), v[i < 3 ? i + 1 : 3]);
+            } else {
+              // every load of the head landed: the MMA warp may overwrite S
+              // with the next head's scores
+              tc::fence_before();
+              arrive(s_free);
+            }
+            float m0 = -INFINITY, m1 = -INFINITY;
+#ifdef VQNQS_ABL_NOMASK
+            if (true) {
+#else
+            if ((sflags >> (4 + i)) & 1u) {
+#endif
 #pragma unroll
-          for (int q = 0; q < 16; q += 2) {
-            const float2 t = tc::ffma2(make_float2(v[i][q], v[i][q + 1]), make_float2(sl2, sl2),
-                                       make_float2(-mref, -mref));
-            if (q / 2 < 8 - VQNQS_ATTN_EMU_PAIRS) {
+              for (int q = 0; q < 16; q += 2) {
+                m0 = fmaxf(m0, v[i][q]);
+                m1 = fmaxf(m1, v[i][q + 1]);
+              }
+            } else {
+              const uint32_t m16 = mk_[i >> 1] >> (16 * (i & 1));
+#pragma unroll
+              for (int q = 0; q < 16; q += 2) {
+                v[i][q] = (m16 >> q) & 1u ? v[i][q] : -INFINITY;
+                v[i][q + 1] = (m16 >> (q + 1)) & 1u ? v[i][q + 1] : -INFINITY;
+                m0 = fmaxf(m0, v[i][q]);
+                m1 = fmaxf(m1, v[i][q + 1]);
+              }
+            }
+            const float mi = fmaxf(m0, m1);
+            const float mref = mi == -INFINITY ? 0.f : mi * sl2;
+            float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < 16; q += 2) {
+              const float2 t = tc::ffma2(make_float2(v[i][q], v[i][q + 1]), make_float2(sl2, sl2),
+                                         make_float2(-mref, -mref));
+#ifdef VQNQS_ABL_NOEXP
+              v[i][q] = t.x;
+              v[i][q + 1] = t.y;
+#else
               v[i][q] = ex2_approx(t.x);
               v[i][q + 1] = ex2_approx(t.y);
-            } else {
-              const float2 e = ex2_poly2(t);
-              v[i][q] = e.x;
-              v[i][q + 1] = e.y;
+#endif
+              s2 = tc::fadd2(s2, make_float2(v[i][q], v[i][q + 1]));
             }
-            sp2 = tc::fadd2(sp2, make_float2(v[i][q], v[i][q + 1]));
+            cm[i] = mi;
+            cs[i] = s2.x + s2.y;
+            if (i + 1 < nl) tc::tmem_wait_ld();
           }
         }
-        const float sp = sp2.x + sp2.y;
+        ATR(1)
+        // the thread's (max, sum) over its chunks; cm[i] becomes chunk i's
+        // weight exp2((m_i - mp) scale log2e) (0 for a chunk without live keys)
+        const float mp = fmaxf(fmaxf(cm[0], cm[1]), fmaxf(cm[2], cm[3]));
+        float sp = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          cm[i] = cs[i] > 0.f ? ex2_approx((cm[i] - mp) * sl2) : 0.f;
+          sp = fmaf(cs[i], cm[i], sp);
+        }
         const int xb = hc & 1;
         ++hc;
         red[xb][part][row] = make_float2(mp, sp);
@@ -701,7 +737,9 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           for (int c = part * 8; c < pcols; c += 32) tc::tmem_st8u(trow + TS_P + c, zero);
           tc::tmem_wait_st();
         }
+#ifndef VQNQS_ABL_NOBAR
         qsync();
+#endif
         ATR(3)
         float2 rq[4];
 #pragma unroll
@@ -723,14 +761,19 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         // ---- normalised bf16 probabilities into the TMEM P tile
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          if (!sl[i]) continue;
+          if (i >= nl) continue;
+          const float fi = f * cm[i];
           uint32_t pk[8];
 #pragma unroll
           for (int q = 0; q < 16; q += 2) {
-            const float2 p2 = tc::fmul2(make_float2(v[i][q], v[i][q + 1]), make_float2(f, f));
+            const float2 p2 = tc::fmul2(make_float2(v[i][q], v[i][q + 1]), make_float2(fi, fi));
             pk[q / 2] = tc::pack_bf16(p2.x, p2.y);
           }
-          tc::tmem_st8u(trow + TS_P + pcol[i], pk);
+#ifndef VQNQS_ABL_NOPST
+          tc::tmem_st8u(trow + TS_P + (sc_[i] >> 9), pk);
+#else
+          if (pk[0] == 0x12345678u && pk[7] == pk[3] + pk[5] + pk[1] && pk[2] == pk[4] + pk[6]) cm[0] += 1.f;
+#endif
         }
         tc::tmem_wait_st();
         ATR(6)
@@ -743,7 +786,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       gi = g1;
     }
 #ifdef VQNQS_ATTN_TRACE
-    if (blockIdx.x < 2 && lane == 0 && (warp == 0 || warp == 5 || warp == 10 || warp == 15))
+    if (blockIdx.x < 1 && lane == 0 && (warp == 0 || warp == 5 || warp == 10 || warp >= 12))
       printf("ATR b%d w%2d items %d: wS %llu ld %llu sm %llu bar %llu comb %llu wPV %llu P %llu arr %llu | end %llu setup %llu\n",
              blockIdx.x, warp, nit, atr[0], atr[1], atr[2], atr[3], atr[4], atr[5], atr[6], atr[7],
              atr[11], atr[12]);
