@@ -116,6 +116,7 @@ extern "C" int vqnqs_debug_tc_attention(int S, int R1, int T, int d, int nh, con
                                         float* rr2) {
   const int dh = d / nh;
   if (!tc_attn_ok(1, d, dh, T)) return 3;
+  const int cap = 256;  // the engine's tile column cap
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int64_t R = int64_t(S) * R1;
@@ -124,7 +125,7 @@ extern "C" int vqnqs_debug_tc_attention(int S, int R1, int T, int d, int nh, con
   int64_t *toff = nullptr, *dM = nullptr;
   AttnTile* tiles = nullptr;
   uint8_t* tinfo = nullptr;
-  const int64_t tcap = R + 16;
+  const int64_t tcap = R + 16;  // every row its own tile at worst
   cudaMalloc(&lrow, M * 4);
   cudaMalloc(&lpos, M * 2);
   cudaMalloc(&tcnt, S * 4);
@@ -136,10 +137,10 @@ extern "C" int vqnqs_debug_tc_attention(int S, int R1, int T, int d, int nh, con
   cudaMemcpy(dM, &M, 8, cudaMemcpyHostToDevice);
   k_enumerate<<<int((R * T + 255) / 256), 256>>>(S, R1, T, K, row_t1, row_aoff, act_off, lrow,
                                                  lpos);
-  k_build_tiles<<<(S + 127) / 128, 128>>>(0, S, R1, T, K, row_t1, row_perm, act_off, tcnt,
+  k_build_tiles<<<(S + 127) / 128, 128>>>(0, S, R1, T, cap, K, row_t1, row_perm, act_off, tcnt,
                                           nullptr, nullptr, tiles, ntiles);
   k_scan<<<1, 1024>>>(S, tcnt, toff, toff + S, 0);
-  k_build_tiles<<<(S + 127) / 128, 128>>>(1, S, R1, T, K, row_t1, row_perm, act_off, tcnt, toff,
+  k_build_tiles<<<(S + 127) / 128, 128>>>(1, S, R1, T, cap, K, row_t1, row_perm, act_off, tcnt, toff,
                                           toff + S, tiles, ntiles);
   k_tile_info<<<sms * 8, 128>>>(tiles, ntiles, R1, T, row_t1, act_off, lrow, lpos, I, Uoff,
                                 tinfo);

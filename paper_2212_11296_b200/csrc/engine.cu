@@ -139,6 +139,7 @@ class EngineImpl {
   bool use_tc_gemm = false;  // tcgen05 per-location GEMMs (bf16)
   bool use_tc_vq = false;    // tcgen05 certified-argmin VQ (both precisions)
   bool use_tc_attn = false;  // tcgen05 gathered attention (bf16)
+  int attn_cap = 256;        // score columns a tile may need (the attention kernel's TMEM budget)
   unsigned long long* d_rescored = nullptr;
   std::vector<void*> allocs;
   float *tok_embed, *pos_embed, *lnf_g, *lnf_b, *head_b;
@@ -542,7 +543,8 @@ class EngineImpl {
     int64_t* tot = tot_.p;  // [0] M total, [1] table total, [2+b] U_b total
     const size_t csmem = k_connected_smem(T, nb);
     smem_optin(reinterpret_cast<const void*>(k_connected), csmem);
-    k_connected<<<(S * 32 + 127) / 128, 128, csmem, st>>>(S, N, g, T, nb, int(dense), d_cfg, d_bonds,
+    k_connected<<<(S * 32 + 127) / 128, 128, csmem, st>>>(S, N, g, T, nb, int(dense), attn_cap,
+                                                      d_cfg, d_bonds,
                                                       K_.p, diag_.p,
                                                       row_bond_.p, row_t1_.p, row_aoff_.p, Mact_.p,
                                                       tok0_.p, attw_.p, row_perm_.p);
@@ -615,17 +617,17 @@ class EngineImpl {
           tiles_.ensure(R);
           tcnt_.ensure(S);
           toff_.ensure(S + 1);
-          k_build_tiles<<<(S + 127) / 128, 128, 0, st>>>(0, S, R1, T, K_.p, row_t1_.p,
+          k_build_tiles<<<(S + 127) / 128, 128, 0, st>>>(0, S, R1, T, attn_cap, K_.p, row_t1_.p,
                                                          row_perm_.p, act_off_.p, tcnt_.p, nullptr,
                                                          nullptr, tiles_.p, ntiles_.p);
           k_scan<<<1, 1024, 0, st>>>(S, tcnt_.p, toff_.p, toff_.p + S, 0);
-          k_build_tiles<<<(S + 127) / 128, 128, 0, st>>>(1, S, R1, T, K_.p, row_t1_.p,
+          k_build_tiles<<<(S + 127) / 128, 128, 0, st>>>(1, S, R1, T, attn_cap, K_.p, row_t1_.p,
                                                          row_perm_.p, act_off_.p, tcnt_.p,
                                                          toff_.p, toff_.p + S, tiles_.p, ntiles_.p);
           launches += 3;
         }
         // per-layer tile tables (qkv rows follow this layer's dedup); at most
-        // 2 M / 128 + 3 S tiles (two consecutive tiles of a sample hold > 128)
+        // 2 M / 128 + 3 S tiles (a tile and the longest row of the next hold > 128)
         const int64_t tcap = std::min<int64_t>(R, M / 64 + 3 * int64_t(S) + 16);
         tinfo_.ensure(size_t(tcap) * TINFO_BYTES);
         k_tile_info<<<sms * 8, 128, 0, st>>>(tiles_.p, ntiles_.p, R1, T, row_t1_.p, act_off_.p,

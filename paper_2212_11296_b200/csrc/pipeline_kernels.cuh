@@ -41,7 +41,7 @@ __device__ __forceinline__ int row_token(const int32_t* tok0, const int32_t* bon
 // per antiparallel bond in bond order (ballot + popc keeps the order).
 // dense != 0 is the no-reuse regime (proj/src/bench.cpp:19-36): every row is
 // active from position 0 (t1 := -1), rows stay in bond order.
-__global__ void k_connected(int S, int N, int g, int T, int nb, int dense,
+__global__ void k_connected(int S, int N, int g, int T, int nb, int dense, int cap,
                             const uint8_t* __restrict__ cfg,
                             const int32_t* __restrict__ bonds, int32_t* __restrict__ K,
                             double* __restrict__ diag, int32_t* __restrict__ row_bond,
@@ -204,18 +204,26 @@ __global__ void k_connected(int S, int N, int g, int T, int nb, int dense,
         ord[e] = t;
       }
     };
+    // a tile's score columns: 16 ceil(max a / 16) base keys + 16 ceil(n / 16)
+    // own keys, at most cap (the attention kernel's TMEM score buffer)
+    auto fits = [&](int c, int amax, int k) {
+      const int n = c + len(k), a = max(amax, T - len(k));
+      return n <= 128 && ((a + 15) & ~15) + ((n + 15) & ~15) <= cap;
+    };
     int i = 0, j = nrows - 1, o = 0;
     while (i <= j) {
       const int o0 = o;
-      int c = len(srt[i]);
+      int c = len(srt[i]), amax = T - c;
       ord[o++] = srt[i++];
-      while (i <= j && c + len(srt[i]) <= 128) {
+      while (i <= j && fits(c, amax, srt[i])) {
         c += len(srt[i]);
+        amax = max(amax, T - len(srt[i]));
         ord[o++] = srt[i++];
       }
       const int om = o;
-      while (j >= i && c + len(srt[j]) <= 128) {
+      while (j >= i && fits(c, amax, srt[j])) {
         c += len(srt[j]);
+        amax = max(amax, T - len(srt[j]));
         ord[o++] = srt[j--];
       }
       if (o0 > 0) {  // [long..., short...] -> [short..., long...], each group's order kept

@@ -58,7 +58,8 @@ struct AttnTile {
 // the tile list. The persistent attention kernel deals tiles round-robin over
 // the CTAs, so the CTAs then work on the same few samples at a time and the
 // samples' shared base-row K/V stay in L2.
-__global__ void k_build_tiles(int pass, int S, int R1, int T, const int32_t* __restrict__ K,
+__global__ void k_build_tiles(int pass, int S, int R1, int T, int cap,
+                              const int32_t* __restrict__ K,
                               const int32_t* __restrict__ row_t1,
                               const int32_t* __restrict__ row_perm,
                               const int64_t* __restrict__ act_off, int32_t* __restrict__ tcnt,
@@ -68,7 +69,7 @@ __global__ void k_build_tiles(int pass, int S, int R1, int T, const int32_t* __r
   if (pass == 1 && s == 0) *n_tiles = (int32_t)*ttot;
   if (s >= S) return;
   const int Ks = K[s];
-  int cur = 0, nt = 0;
+  int cur = 0, nt = 0, amax = 0;
   bool cut = false;
   int64_t start = act_off[s];
   const int64_t base = pass == 1 ? toff[s] : 0;
@@ -78,13 +79,17 @@ __global__ void k_build_tiles(int pass, int S, int R1, int T, const int32_t* __r
     const int n = k == 0 ? T : T - (row_t1[(int64_t)s * R1 + k] + 1);
     cut |= kf != k;
     if (n <= 0) continue;
-    if (cur + n > 128 || (cut && cur > 0)) {
+    // score columns of the tile: base keys up to the largest a, then own keys
+    const int cols = ((max(amax, T - n) + 15) & ~15) + ((cur + n + 15) & ~15);
+    if (cur > 0 && (cur + n > 128 || cols > cap || cut)) {
       if (pass == 1) tiles[base + nt] = AttnTile{s, cur, start};
       ++nt;
       start += cur;
       cur = 0;
+      amax = 0;
     }
     cur += n;
+    amax = max(amax, T - n);
     cut = false;
   }
   if (cur > 0) {
@@ -172,12 +177,23 @@ struct AttnSmem {
   }
 };
 
-#ifdef VQNQS_ATTN_TRACE
+#if defined(VQNQS_ATTN_TL)
+// timeline mode: raw clock() of every trace point for three consecutive heads
+#define VQNQS_TL_H0 (200 + 24 * (int)blockIdx.x)
+#define ATR_DECL int tl_h = -1;
+#define ATR(k) { if ((unsigned)tl_h < 3u) tlog[warp][tl_h * 12 + (k)] = (unsigned)clock(); }
+#define MTR_DECL int tl_h = -VQNQS_TL_H0 - 1;
+#define MTR(k) ATR(k)
+#elif defined(VQNQS_ATTN_TRACE)
 #define ATR_DECL unsigned long long atr[16] = {0}; long long atr_t = clock64();
 #define ATR(k) { const long long _n = clock64(); atr[k] += _n - atr_t; atr_t = _n; }
+#define MTR_DECL unsigned mtr[8] = {0}; unsigned mtr_t = (unsigned)clock();
+#define MTR(k) { const unsigned _n = (unsigned)clock(); mtr[k] += _n - mtr_t; mtr_t = _n; }
 #else
 #define ATR_DECL
 #define ATR(k)
+#define MTR_DECL
+#define MTR(k)
 #endif
 
 // exp2 of a pair on the FMA pipe, for moving part of the softmax exponentials
@@ -188,6 +204,9 @@ struct AttnSmem {
 // masked entries, t = -inf). VQNQS_ATTN_EMU_PAIRS of the 8 pairs per score
 // chunk take this path; measured on c4 / c5 0 is as fast as 2
 // and faster than 3 or 4: the softmax warps are latency-, not MUFU-bound.
+#ifndef VQNQS_ATTN_SWP
+#define VQNQS_ATTN_SWP 1
+#endif
 #ifndef VQNQS_ATTN_EMU_PAIRS
 #define VQNQS_ATTN_EMU_PAIRS 0
 #endif
@@ -233,9 +252,16 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // value MMA); and the MMA warpgroup (warp 24 issues every tcgen05.mma, warps
 // 25-27 stage the operands with cp.async). setmaxnreg redistributes the
 // 896 x 72 launch registers: softmax 96, drain 40, MMA / producers 32.
-constexpr int TCA_SOFTMAX_WARPS = 16;
-constexpr int TCA_DRAIN_WARP0 = 16;
-constexpr int TCA_DRAIN_WARPS = 8;  // two per row quadrant, 32 columns each
+#ifndef VQNQS_TCA_PARTS
+#define VQNQS_TCA_PARTS 4
+#endif
+constexpr int TCA_PARTS = VQNQS_TCA_PARTS;  // softmax warps per row quadrant (they split its score chunks)
+constexpr int TCA_SLOTS = (16 + TCA_PARTS - 1) / TCA_PARTS;  // chunks per softmax warp
+static_assert(TCA_PARTS == 4 || TCA_PARTS == 6, "softmax warps per quadrant");
+constexpr int TCA_SOFTMAX_WARPS = 4 * TCA_PARTS;
+constexpr int TCA_SOFTMAX_REGS = TCA_PARTS == 6 ? 72 : 96;
+constexpr int TCA_DRAIN_WARP0 = TCA_SOFTMAX_WARPS;
+constexpr int TCA_DRAIN_WARPS = TCA_PARTS == 6 ? 4 : 8;  // per row quadrant: 64 / 32 columns each
 constexpr int TCA_DRAIN_COLS = 64 * 4 / TCA_DRAIN_WARPS;
 constexpr int TCA_MMA_WARP = TCA_DRAIN_WARP0 + TCA_DRAIN_WARPS;
 constexpr int TCA_THREADS = 32 * (TCA_MMA_WARP + 4);
@@ -265,10 +291,14 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 18);
   // exchange buffers alternate by head: a fast warp may publish head h+1
   // before a slow one of its quadrant has read head h
-  __shared__ float2 red[2][4][128];  // (local max, local sum)
+  __shared__ float2 red[2][TCA_PARTS][128];  // (local max, local sum)
   __shared__ float2 dnrm[128];       // drain warps' partial row norms
+#ifdef VQNQS_ATTN_TL
+  __shared__ unsigned tlog[32][36];
+  for (int i = threadIdx.x; i < 32 * 36; i += blockDim.x) (&tlog[0][0])[i] = 0;
+#endif
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int row = tid & 127, part = (tid >> 7) & 3;  // warp w owns TMEM lanes 32(w%4)..
+  const int row = tid & 127, part = tid >> 7;  // warp w owns TMEM lanes 32(w%4)..
   const int KBb = attn_kb_base(T);
   const int n_tiles = *n_tiles_p;
   const int TP = attn_tpad(T);
@@ -455,6 +485,10 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         __syncwarp();
       };
       uint32_t ph_free = 0, ph_p = 0;
+      MTR_DECL
+#ifdef VQNQS_ATTN_TRACE2
+      uint32_t ph_sf = 1;  // S(0)'s phase is not waited for here
+#endif
       // S(0)
       tc::mbar_wait(&st_full[0], 0);
       tc::fence_after();
@@ -473,24 +507,40 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           }
         }
         int kb_next = kb_cur, no_next = no_cur;
+        MTR(0)
+#ifdef VQNQS_ATTN_TL
+        ++tl_h;
+        MTR(8)
+#endif
         if (it2 < nit) {
           tc::mbar_wait(s_free, ph_free);  // every warp holds S(g)
           ph_free ^= 1;
+          MTR(1)
           if (it2 != it) {
             tc::mbar_wait(&st_full[it2 & 1], (it2 >> 1) & 1);  // operands of item it2
             kb_next = kb_of(j2);
             no_next = own_of(j2);
           }
           tc::fence_after();
+          MTR(2)
           issue_scores(it2, hh2, kb_next, no_next);
+          MTR(3)
+#ifdef VQNQS_ATTN_TRACE2
+          tc::mbar_wait(s_full, ph_sf);
+          ph_sf ^= 1;
+          MTR(7)
+#endif
         }
         if (hh == 0 && it >= 2) {
           tc::mbar_wait(&o_empty[it & 1], ((it - 2) >> 1) & 1);  // O buffer drained
         }
+        MTR(4)
         tc::mbar_wait(p_full, ph_p);  // every warp wrote P(g)
         ph_p ^= 1;
         tc::fence_after();
+        MTR(5)
         issue_pv(it, hh, kb_cur, no_cur);
+        MTR(6)
         if (hh == hpg - 1) {  // item it's operands read
           if (leader) tc::mma_commit(&stage_free[it & 1]);
           __syncwarp();
@@ -503,6 +553,11 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         kb_cur = kb_next;
         no_cur = no_next;
       }
+#if defined(VQNQS_ATTN_TRACE) && !defined(VQNQS_ATTN_TL)
+      if (blockIdx.x < 1 && lane == 0)
+        printf("ATR-MMA b%d items %d: loop %u w_sfree %u w_stfull %u issueS %u w_oempty %u w_pfull %u issuePV %u S-latency %u\n",
+               blockIdx.x, nit, mtr[0], mtr[1], mtr[2], mtr[3], mtr[4], mtr[5], mtr[6], mtr[7]);
+#endif
     }
     if (warp > TCA_MMA_WARP && nit > 0) {
       // ================= producer warps: cp.async staging of every item into
@@ -569,11 +624,11 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     }
   } else {
     // ================= softmax / epilogue warps
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 96;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(TCA_SOFTMAX_REGS) : "memory");
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const float sl2 = scale * 1.4426950408889634f;
     const uint32_t qbar = 1 + (warp & 3);  // named barrier of the row quadrant (128 threads)
-    auto qsync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory"); };
+    auto qsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(qbar), "n"(32 * TCA_PARTS) : "memory"); };
     auto arrive = [&](uint64_t* b) {  // one arrival per warp
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(b));
@@ -588,13 +643,17 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     //   sc_[i] = S column | P column << 9; mk_[i >> 1] bits 16 (i & 1) + j:
     //   entry j of the chunk is a key of the lane's row; sflags bit i: slot
     //   live, bit 4 + i: every live row uses the whole chunk
-    uint32_t sc_[4] = {0, 0, 0, 0}, mk_[2] = {0, 0}, sflags = 0;
+    uint32_t sc_[TCA_SLOTS], mk_[2] = {0, 0}, sflags = 0;
+#pragma unroll
+    for (int i = 0; i < TCA_SLOTS; ++i) sc_[i] = 0;
     int j = 0, gi = 0;  // item it = (j, gi)
     for (int it = 0; it < nit; ++it) {
       const int j1 = gi + 1 == G ? j + 1 : j, g1 = gi + 1 == G ? 0 : gi + 1;  // item it + 1
       if (gi == 0) {
         // the table landed before any warp signalled this item's operands
+        ATR(13)
         tc::mbar_wait(&st_full[it & 1], (it >> 1) & 1);
+        ATR(9)
         const uint8_t* ti = slot(j);
         live = row < reinterpret_cast<const int32_t*>(ti + 1544)[0];
         const int a = reinterpret_cast<const int16_t*>(ti + 1024)[row];
@@ -611,8 +670,8 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         sflags = 0;
         mk_[0] = mk_[1] = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int q = part + 4 * i;
+        for (int i = 0; i < TCA_SLOTS; ++i) {
+          const int q = part + TCA_PARTS * i;
           const bool isb = q < nb;
           const int c0 = isb ? 16 * q : wo_beg + 16 * (q - nb);
           const int off = isb ? c0 : c0 - own_lo;
@@ -629,10 +688,18 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       }
       ATR(12)
       for (int hh = 0; hh < hpg; ++hh) {
+#ifdef VQNQS_ATTN_TL
+        tl_h = (int)hc - VQNQS_TL_H0;
+        ATR(9)
+#endif
         tc::mbar_wait(s_full, ph_s);
         ph_s ^= 1;
         tc::fence_after();
+#if defined(VQNQS_ATTN_TL)
         ATR(0)
+#elif defined(VQNQS_ATTN_TRACE)
+        if (hh == 0) ATR(8) else ATR(0)
+#endif
         // ---- the warp's live 16-column chunks (base chunks, then own chunks)
         // are dealt round-robin to the four warpgroups: slot i is chunk
         // part + 4i, live slots are a prefix. Each chunk is processed on its
@@ -644,9 +711,100 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         // chunks first, the four ran both phases in lockstep). The per-chunk
         // references are folded into the row's normaliser below, like the
         // per-warp ones.
-        float v[4][16];
-        float cm[4], cs[4];
+        float v[TCA_SLOTS][16];
+        float cm[TCA_SLOTS], cs[TCA_SLOTS];
         const int nl = __popc(sflags & 15u);
+#ifdef VQNQS_ATTN_TL
+        if ((unsigned)tl_h < 3u) tlog[warp][tl_h * 12 + 11] = 1000u + nl * 100 + (sflags >> 4);
+#endif
+#if VQNQS_ATTN_SWP
+        // Software pipeline inside the warp: chunk i + 1 is masked and reduced
+        // to its max (ALU pipe) in the same straight-line block as chunk i's
+        // exponentials (MUFU) and chunk i + 2's TMEM load, one block per live
+        // chunk count, so the two pipes overlap within a warp instead of the
+        // quadrant's four warps saturating first one and then the other.
+#pragma unroll
+        for (int i = 0; i < TCA_SLOTS; ++i) {
+          cm[i] = -INFINITY;
+          cs[i] = 0.f;
+        }
+        auto maskmax = [&](auto ic) {
+          constexpr int i = decltype(ic)::value;
+          const uint32_t m16 = mk_[i >> 1] >> (16 * (i & 1));
+          float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+          for (int q = 0; q < 16; q += 2) {
+#ifndef VQNQS_ABL_NOMASK
+            v[i][q] = (m16 >> q) & 1u ? v[i][q] : -INFINITY;
+            v[i][q + 1] = (m16 >> (q + 1)) & 1u ? v[i][q + 1] : -INFINITY;
+#endif
+            m0 = fmaxf(m0, v[i][q]);
+            m1 = fmaxf(m1, v[i][q + 1]);
+          }
+          cm[i] = fmaxf(m0, m1);
+        };
+        auto exps = [&](auto ic) {
+          constexpr int i = decltype(ic)::value;
+          const float mref = cm[i] == -INFINITY ? 0.f : cm[i] * sl2;
+          float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < 16; q += 2) {
+            const float2 t = tc::ffma2(make_float2(v[i][q], v[i][q + 1]), make_float2(sl2, sl2),
+                                       make_float2(-mref, -mref));
+            if (q / 2 < VQNQS_ATTN_EMU_PAIRS) {
+              const float2 e = ex2_poly2(t);
+              v[i][q] = e.x;
+              v[i][q + 1] = e.y;
+            } else {
+#ifdef VQNQS_ABL_NOEXP
+              v[i][q] = t.x;
+              v[i][q + 1] = t.y;
+#else
+              v[i][q] = ex2_approx(t.x);
+              v[i][q + 1] = ex2_approx(t.y);
+#endif
+            }
+            s2 = tc::fadd2(s2, make_float2(v[i][q], v[i][q + 1]));
+          }
+          cs[i] = s2.x + s2.y;
+        };
+        auto s_loaded = [&]() {
+          // every load of the head landed: the MMA warp may overwrite S with
+          // the next head's scores
+          tc::fence_before();
+          arrive(s_free);
+#ifdef VQNQS_ATTN_TL
+          ATR(10)
+#endif
+        };
+        auto run = [&](auto nlc) {
+          constexpr int NL = decltype(nlc)::value;
+          tc::tmem_ld16(trow + (sc_[0] & 511u), v[0]);
+          if constexpr (NL > 1) tc::tmem_ld16(trow + (sc_[1] & 511u), v[1]);
+          tc::tmem_wait_ld();
+          if constexpr (NL <= 2) s_loaded();
+          maskmax(std::integral_constant<int, 0>{});
+          tc::static_for<NL>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            if constexpr (i + 2 < NL) tc::tmem_ld16(trow + (sc_[i + 2] & 511u), v[i + 2]);
+            if constexpr (i + 1 < NL) maskmax(std::integral_constant<int, i + 1>{});
+            exps(ic);
+            if constexpr (i + 2 < NL) {
+              tc::tmem_wait_ld();
+              if constexpr (i + 2 == NL - 1) s_loaded();
+            }
+          });
+        };
+        switch (nl) {
+          case 0: s_loaded(); break;
+          case 1: run(std::integral_constant<int, 1>{}); break;
+          case 2: run(std::integral_constant<int, 2>{}); break;
+          case 3: run(std::integral_constant<int, 3>{}); break;
+          default:
+            if constexpr (TCA_SLOTS >= 4) run(std::integral_constant<int, TCA_SLOTS>{});
+            break;
+        }
+#else
         if (nl > 0) tc::tmem_ld16(trow + (sc_[0] & 511u), v[0]);
         tc::tmem_wait_ld();
         if (nl == 0) {
@@ -654,24 +812,24 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           arrive(s_free);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < TCA_SLOTS; ++i) {
           cm[i] = -INFINITY;
           cs[i] = 0.f;
           if (i < nl) {
             if (i + 1 < nl) {
-              if (i < 3) tc::tmem_ld16(trow + (sc_[i < 3 ? i + 1 : 3] & 511u), v[i < 3 ? i + 1 : 3]);
+              constexpr int L = TCA_SLOTS - 1;
+              if (i < L) tc::tmem_ld16(trow + (sc_[i < L ? i + 1 : L] & 511u), v[i < L ? i + 1 : L]);
             } else {
               // every load of the head landed: the MMA warp may overwrite S
               // with the next head's scores
               tc::fence_before();
               arrive(s_free);
+#ifdef VQNQS_ATTN_TL
+              ATR(10)
+#endif
             }
             float m0 = -INFINITY, m1 = -INFINITY;
-#ifdef VQNQS_ABL_NOMASK
-            if (true) {
-#else
             if ((sflags >> (4 + i)) & 1u) {
-#endif
 #pragma unroll
               for (int q = 0; q < 16; q += 2) {
                 m0 = fmaxf(m0, v[i][q]);
@@ -694,13 +852,14 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
             for (int q = 0; q < 16; q += 2) {
               const float2 t = tc::ffma2(make_float2(v[i][q], v[i][q + 1]), make_float2(sl2, sl2),
                                          make_float2(-mref, -mref));
-#ifdef VQNQS_ABL_NOEXP
-              v[i][q] = t.x;
-              v[i][q + 1] = t.y;
-#else
-              v[i][q] = ex2_approx(t.x);
-              v[i][q + 1] = ex2_approx(t.y);
-#endif
+              if (q / 2 < VQNQS_ATTN_EMU_PAIRS) {
+                const float2 e = ex2_poly2(t);
+                v[i][q] = e.x;
+                v[i][q + 1] = e.y;
+              } else {
+                v[i][q] = ex2_approx(t.x);
+                v[i][q + 1] = ex2_approx(t.y);
+              }
               s2 = tc::fadd2(s2, make_float2(v[i][q], v[i][q + 1]));
             }
             cm[i] = mi;
@@ -708,13 +867,16 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
             if (i + 1 < nl) tc::tmem_wait_ld();
           }
         }
+#endif
         ATR(1)
         // the thread's (max, sum) over its chunks; cm[i] becomes chunk i's
         // weight exp2((m_i - mp) scale log2e) (0 for a chunk without live keys)
-        const float mp = fmaxf(fmaxf(cm[0], cm[1]), fmaxf(cm[2], cm[3]));
+        float mp = cm[0];
+#pragma unroll
+        for (int i = 1; i < TCA_SLOTS; ++i) mp = fmaxf(mp, cm[i]);
         float sp = 0.f;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < TCA_SLOTS; ++i) {
           cm[i] = cs[i] > 0.f ? ex2_approx((cm[i] - mp) * sl2) : 0.f;
           sp = fmaf(cs[i], cm[i], sp);
         }
@@ -734,20 +896,20 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           // quadrant barrier: another warpgroup may write these columns)
           const int pcols = (kb_base + 128) / 2;
           const uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          for (int c = part * 8; c < pcols; c += 32) tc::tmem_st8u(trow + TS_P + c, zero);
+          for (int c = part * 8; c < pcols; c += 8 * TCA_PARTS) tc::tmem_st8u(trow + TS_P + c, zero);
           tc::tmem_wait_st();
         }
-#ifndef VQNQS_ABL_NOBAR
         qsync();
-#endif
         ATR(3)
-        float2 rq[4];
+        float2 rq[TCA_PARTS];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) rq[q] = red[xb][q][row];
-        const float m = fmaxf(fmaxf(rq[0].x, rq[1].x), fmaxf(rq[2].x, rq[3].x));
+        for (int q = 0; q < TCA_PARTS; ++q) rq[q] = red[xb][q][row];
+        float m = rq[0].x;
+#pragma unroll
+        for (int q = 1; q < TCA_PARTS; ++q) m = fmaxf(m, rq[q].x);
         float tot = 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < TCA_PARTS; ++q)
           tot += rq[q].y > 0.f ? rq[q].y * ex2_approx((rq[q].x - m) * sl2) : 0.f;
         const float f = sp > 0.f ? __fdividef(ex2_approx((mp - m) * sl2), tot) : 0.f;
         ATR(4)
@@ -760,7 +922,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         ATR(5)
         // ---- normalised bf16 probabilities into the TMEM P tile
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < TCA_SLOTS; ++i) {
           if (i >= nl) continue;
           const float fi = f * cm[i];
           uint32_t pk[8];
@@ -769,11 +931,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
             const float2 p2 = tc::fmul2(make_float2(v[i][q], v[i][q + 1]), make_float2(fi, fi));
             pk[q / 2] = tc::pack_bf16(p2.x, p2.y);
           }
-#ifndef VQNQS_ABL_NOPST
           tc::tmem_st8u(trow + TS_P + (sc_[i] >> 9), pk);
-#else
-          if (pk[0] == 0x12345678u && pk[7] == pk[3] + pk[5] + pk[1] && pk[2] == pk[4] + pk[6]) cm[0] += 1.f;
-#endif
         }
         tc::tmem_wait_st();
         ATR(6)
@@ -785,15 +943,30 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       j = j1;
       gi = g1;
     }
-#ifdef VQNQS_ATTN_TRACE
+#if defined(VQNQS_ATTN_TRACE) && !defined(VQNQS_ATTN_TL)
     if (blockIdx.x < 1 && lane == 0 && (warp == 0 || warp == 5 || warp == 10 || warp >= 12))
-      printf("ATR b%d w%2d items %d: wS %llu ld %llu sm %llu bar %llu comb %llu wPV %llu P %llu arr %llu | end %llu setup %llu\n",
+      printf("ATR b%d w%2d items %d: wS %llu ld %llu sm %llu bar %llu comb %llu wPV %llu P %llu arr %llu | end %llu setup %llu | wS(h0) %llu wST %llu\n",
              blockIdx.x, warp, nit, atr[0], atr[1], atr[2], atr[3], atr[4], atr[5], atr[6], atr[7],
-             atr[11], atr[12]);
+             atr[11], atr[12], atr[8], atr[9]);
 #endif
   }
   tc::fence_before();
   __syncthreads();
+#ifdef VQNQS_ATTN_TL
+  if (blockIdx.x < 8 && tid == 0 && nit * hpg > VQNQS_TL_H0 + 3) {
+    unsigned t0 = 0xffffffffu;
+    for (int w = 0; w < 32; ++w)
+      for (int e = 0; e < 36; ++e)
+        if (tlog[w][e] && tlog[w][e] < t0) t0 = tlog[w][e];
+    for (int w = 0; w < 32; ++w)
+      for (int h = 0; h < 3; ++h) {
+        unsigned e[12];
+        for (int k = 0; k < 12; ++k) e[k] = tlog[w][h * 12 + k] ? tlog[w][h * 12 + k] - (k == 11 ? 0 : t0) : 0u;
+        printf("TL %d %d %d %u %u %u %u %u %u %u %u %u %u %u %u\n", (int)blockIdx.x, w, h, e[0], e[1],
+               e[2], e[3], e[4], e[5], e[6], e[7], e[8], e[9], e[10], e[11]);
+      }
+  }
+#endif
   if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
 

@@ -8,6 +8,8 @@
 // advancing K by 16 elements inside the 128-byte row adds 32 bytes to the
 // start address.
 #pragma once
+#include <utility>
+#include <type_traits>
 
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -108,6 +110,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+// compile-time loop: f(std::integral_constant<int, 0>{}) ... f(<N - 1>)
+template <class F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
