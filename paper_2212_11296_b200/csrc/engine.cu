@@ -606,7 +606,7 @@ class EngineImpl {
       TA* h = reinterpret_cast<TA*>(h_.p);
       TA* qkv = reinterpret_cast<TA*>(qkv_.p);
       TA* f1 = reinterpret_cast<TA*>(f1_.p);
-      k_layernorm<TA><<<lnGrid, 256, 0, st>>>(Mb, d, xcur, B.ln1_g, B.ln1_b, h);
+      launch_layernorm<TA>(lnGrid, st, Mb, d, xcur, B.ln1_g, B.ln1_b, h);
       ++launches;
       gemm<TA>(Mb, M, 3 * d, d, h, d, nullptr, B.wqkv, B.wqkvT, B.bqkv, qkv, 3 * d, EPI_STORE,
                nullptr, 0, nullptr, st);
@@ -709,7 +709,7 @@ class EngineImpl {
         launches += 3;
         // continuation (proj/src/dedup.cpp:246-267): y = r + (code rows Wo + bo)
         // from the per-code tables, fused with LN2
-        k_cont_ln<TA><<<lnGrid, 256, 0, st>>>(Mn, d, H, Q, xcur, g_res_.p, g_code_.p, B.pwo,
+        launch_cont_ln<TA>(lnGrid, st, Mn, d, H, Q, xcur, g_res_.p, g_code_.p, B.pwo,
                                               B.ln2_g, B.ln2_b, ybuf, h);
         ++launches;
         gemm<TA>(Mn, M, 4 * d, d, h, d, nullptr, B.w1, B.w1T, B.b1, f1, 4 * d, EPI_GELU, nullptr,
@@ -743,7 +743,7 @@ class EngineImpl {
         gemm<TA>(Mn, M, d, d, A, d, nullptr, B.wo, B.woT, B.bo, xnext, d, EPI_RESID, ybuf, d,
                  nullptr, st);
         if (B.has_ffn) {
-          k_layernorm<TA><<<lnGrid, 256, 0, st>>>(Mn, d, xnext, B.ln2_g, B.ln2_b, h);
+          launch_layernorm<TA>(lnGrid, st, Mn, d, xnext, B.ln2_g, B.ln2_b, h);
           ++launches;
           gemm<TA>(Mn, M, 4 * d, d, h, d, nullptr, B.w1, B.w1T, B.b1, f1, 4 * d, EPI_GELU,
                    nullptr, 0, nullptr, st);
@@ -762,7 +762,7 @@ class EngineImpl {
     // (e) head and E_loc
     const int64_t* ML = tot + 2 + L;
     TA* h = reinterpret_cast<TA*>(h_.p);
-    k_layernorm<TA><<<lnGrid, 256, 0, st>>>(ML, d, xcur, lnf_g, lnf_b, h);
+    launch_layernorm<TA>(lnGrid, st, ML, d, xcur, lnf_g, lnf_b, h);
     k_head<TA><<<lnGrid, 256, 0, st>>>(ML, d, V, lastV, T, h, static_cast<const TA*>(head_w),
                                        head_b, upos_.p, lpV_.p);
     double* lp_rows = nullptr;
@@ -958,7 +958,7 @@ class EngineImpl {
       float* xn = ya.p;
       for (int b = 0; b < L; ++b) {
         const DevBlock& Bk = blk[b];
-        k_layernorm<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, xc, Bk.ln1_g, Bk.ln1_b, hp);
+        launch_layernorm<TA>(lnGrid, st, dB.p, d, xc, Bk.ln1_g, Bk.ln1_b, hp);
         gemm<TA>(dB.p, B, 3 * d, d, hp, d, nullptr, Bk.wqkv, Bk.wqkvT, Bk.bqkv, qp, 3 * d,
                  EPI_STORE, nullptr, 0, nullptr, st);
         TA* kcb = reinterpret_cast<TA*>(kc.p) + size_t(b) * B * T * d;
@@ -979,7 +979,7 @@ class EngineImpl {
           gemm<TA>(dB.p, B, d, d, A, d, nullptr, Bk.wo, Bk.woT, Bk.bo, xn, d, EPI_RESID, xc, d,
                    nullptr, st);
           if (Bk.has_ffn) {
-            k_layernorm<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, xn, Bk.ln2_g, Bk.ln2_b, hp);
+            launch_layernorm<TA>(lnGrid, st, dB.p, d, xn, Bk.ln2_g, Bk.ln2_b, hp);
             ++launches;
             gemm<TA>(dB.p, B, 4 * d, d, hp, d, nullptr, Bk.w1, Bk.w1T, Bk.b1, fp, 4 * d,
                      EPI_GELU, nullptr, 0, nullptr, st);
@@ -999,7 +999,7 @@ class EngineImpl {
           vq_simt(dB.p, B, att.p, Bk.cb32, code.p, st);
         }
         // continuation (proj/src/dedup.cpp:246-267) from the per-code Wo tables
-        k_cont_ln<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, H, Q, xc, iota.p, code.p, Bk.pwo, Bk.ln2_g,
+        launch_cont_ln<TA>(lnGrid, st, dB.p, d, H, Q, xc, iota.p, code.p, Bk.pwo, Bk.ln2_g,
                                               Bk.ln2_b, y_.p, hp);
         ++launches;
         gemm<TA>(dB.p, B, 4 * d, d, hp, d, nullptr, Bk.w1, Bk.w1T, Bk.b1, fp, 4 * d, EPI_GELU,
@@ -1008,7 +1008,7 @@ class EngineImpl {
                  y_.p, d, nullptr, st);
         std::swap(xc, xn);
       }
-      k_layernorm<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, xc, lnf_g, lnf_b, hp);
+      launch_layernorm<TA>(lnGrid, st, dB.p, d, xc, lnf_g, lnf_b, hp);
       k_head<TA><<<lnGrid, 256, 0, st>>>(dB.p, d, V, lastV, T, hp, static_cast<const TA*>(head_w),
                                          head_b, pos.p, lpv.p);
       k_dec_sample<<<(B + 127) / 128, 128, 0, st>>>(B, T, V, t, lpv.p, d_u, d_tok, d_lp);

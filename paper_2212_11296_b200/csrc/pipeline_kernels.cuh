@@ -723,6 +723,122 @@ __global__ void k_layernorm(const int64_t* __restrict__ Mp, int d, const float* 
   }
 }
 
+// d = 128 NV: the row as NV float4 per lane (element 4 lane + 128 k ..), read
+// once with 512-byte warp loads, the warp's next row in flight; statistics in
+// double as above ((double)x - mean is the deviation of both later passes), the
+// affine output (t rstd) gamma + beta in fp32 from the double t rstd: two
+// conversions per element instead of six, which bound the scalar kernel.
+template <typename TA>
+__device__ __forceinline__ void store4(TA* p, float a, float b, float c, float e);
+template <>
+__device__ __forceinline__ void store4<float>(float* p, float a, float b, float c, float e) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, e);
+}
+template <>
+__device__ __forceinline__ void store4<bf16>(bf16* p, float a, float b, float c, float e) {
+  const __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, e);
+  uint2 w;
+  w.x = *reinterpret_cast<const uint32_t*>(&lo);
+  w.y = *reinterpret_cast<const uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = w;
+}
+
+// statistics and output of one row held as NV float4 per lane
+template <typename TA, int NV>
+__device__ __forceinline__ void ln_row_v(const float4* xv, int lane, const float* __restrict__ gam,
+                                         const float* __restrict__ bet, TA* __restrict__ orow) {
+  constexpr int d = 128 * NV;
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    s += ((double)xv[k].x + (double)xv[k].y) + ((double)xv[k].z + (double)xv[k].w);
+  const double mean = warp_sum(s) / d;
+  double q = 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double t0 = xv[k].x - mean, t1 = xv[k].y - mean, t2 = xv[k].z - mean,
+                 t3 = xv[k].w - mean;
+    q += (t0 * t0 + t1 * t1) + (t2 * t2 + t3 * t3);
+  }
+  const double var = warp_sum(q) / d;
+  const double rstd = 1.0 / sqrt(var + 1e-5);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = 4 * lane + 128 * k;
+    const float4 g = *reinterpret_cast<const float4*>(gam + c);
+    const float4 b = *reinterpret_cast<const float4*>(bet + c);
+    store4<TA>(orow + c, fmaf((float)((xv[k].x - mean) * rstd), g.x, b.x),
+               fmaf((float)((xv[k].y - mean) * rstd), g.y, b.y),
+               fmaf((float)((xv[k].z - mean) * rstd), g.z, b.z),
+               fmaf((float)((xv[k].w - mean) * rstd), g.w, b.w));
+  }
+}
+
+template <typename TA, int NV>
+__global__ void __launch_bounds__(256) k_layernorm_v(const int64_t* __restrict__ Mp,
+                                                     const float* __restrict__ x,
+                                                     const float* __restrict__ gam,
+                                                     const float* __restrict__ bet,
+                                                     TA* __restrict__ out) {
+  constexpr int d = 128 * NV;
+  const int64_t M = *Mp;
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  const int64_t r0 = blockIdx.x * wpb + (threadIdx.x >> 5), rstep = (int64_t)gridDim.x * wpb;
+  float4 nx[NV];
+  auto load = [&](int64_t r) {
+    const float4* xr = reinterpret_cast<const float4*>(x + (r < M ? r : 0) * d);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) nx[k] = xr[lane + 32 * k];
+  };
+  load(r0);
+  for (int64_t r = r0; r < M; r += rstep) {
+    float4 xv[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) xv[k] = nx[k];
+    load(r + rstep);
+    ln_row_v<TA, NV>(xv, lane, gam, bet, out + r * d);
+  }
+}
+
+// k_cont_ln for one VQ head and d = 128 NV (see k_cont_ln below)
+template <typename TA, int NV>
+__global__ void __launch_bounds__(256) k_cont_ln_v(
+    const int64_t* __restrict__ Mp, const float* __restrict__ x,
+    const int64_t* __restrict__ g_res, const int32_t* __restrict__ g_code,
+    const float* __restrict__ pwo, const float* __restrict__ gam, const float* __restrict__ bet,
+    float* __restrict__ y, TA* __restrict__ out) {
+  constexpr int d = 128 * NV;
+  const int64_t M = *Mp;
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  const int64_t r0 = blockIdx.x * wpb + (threadIdx.x >> 5), rstep = (int64_t)gridDim.x * wpb;
+  float4 nx[NV], np[NV];
+  auto gather = [&](int64_t r) {
+    const bool ok = r < M;
+    const float4* xr = reinterpret_cast<const float4*>(x + (ok ? g_res[r] : 0) * d);
+    const float4* pr = reinterpret_cast<const float4*>(pwo + (int64_t)(ok ? g_code[r] : 0) * d);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      nx[k] = xr[lane + 32 * k];
+      np[k] = pr[lane + 32 * k];
+    }
+  };
+  gather(r0);
+  for (int64_t r = r0; r < M; r += rstep) {
+    float4 yv[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      yv[k] = make_float4(nx[k].x + np[k].x, nx[k].y + np[k].y, nx[k].z + np[k].z,
+                          nx[k].w + np[k].w);
+    gather(r + rstep);
+    float4* yr = reinterpret_cast<float4*>(y + r * d);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) yr[lane + 32 * k] = yv[k];
+    ln_row_v<TA, NV>(yv, lane, gam, bet, out + r * d);
+  }
+}
+
 // Continuation head (proj/src/dedup.cpp:255-262) on the U_{b+1} new unique
 // rows: y = r + o with r the block-input residual row and o = code_row Wo + bo
 // read from the per-code table pwo (computed once per model by the same GEMM,
@@ -831,6 +947,38 @@ __global__ void k_cont_ln(const int64_t* __restrict__ Mp, int d, int H, int Q,
     const double rstd = 1.0 / sqrt(var + 1e-5);
     for (int c = lane; c < d; c += 32)
       out[r * d + c] = from_f<TA>((float)((yr[c] - mean) * rstd * gam[c] + bet[c]));
+  }
+}
+
+// LayerNorm / continuation launchers: the vector kernels for d = 128 NV,
+// NV in {1, 2, 3, 4, 6, 8}; the scalar ones otherwise.
+template <typename TA>
+inline void launch_layernorm(int grid, cudaStream_t st, const int64_t* Mp, int d, const float* x,
+                             const float* gam, const float* bet, TA* out) {
+  switch (d % 128 == 0 ? d / 128 : 0) {
+    case 1: k_layernorm_v<TA, 1><<<grid, 256, 0, st>>>(Mp, x, gam, bet, out); break;
+    case 2: k_layernorm_v<TA, 2><<<grid, 256, 0, st>>>(Mp, x, gam, bet, out); break;
+    case 3: k_layernorm_v<TA, 3><<<grid, 256, 0, st>>>(Mp, x, gam, bet, out); break;
+    case 4: k_layernorm_v<TA, 4><<<grid, 256, 0, st>>>(Mp, x, gam, bet, out); break;
+    case 6: k_layernorm_v<TA, 6><<<grid, 256, 0, st>>>(Mp, x, gam, bet, out); break;
+    case 8: k_layernorm_v<TA, 8><<<grid, 256, 0, st>>>(Mp, x, gam, bet, out); break;
+    default: k_layernorm<TA><<<grid, 256, 0, st>>>(Mp, d, x, gam, bet, out);
+  }
+}
+template <typename TA>
+inline void launch_cont_ln(int grid, cudaStream_t st, const int64_t* Mp, int d, int H, int Q,
+                           const float* x, const int64_t* g_res, const int32_t* g_code,
+                           const float* pwo, const float* gam, const float* bet, float* y,
+                           TA* out) {
+  switch (H == 1 && d % 128 == 0 ? d / 128 : 0) {
+    case 1: k_cont_ln_v<TA, 1><<<grid, 256, 0, st>>>(Mp, x, g_res, g_code, pwo, gam, bet, y, out); break;
+    case 2: k_cont_ln_v<TA, 2><<<grid, 256, 0, st>>>(Mp, x, g_res, g_code, pwo, gam, bet, y, out); break;
+    case 3: k_cont_ln_v<TA, 3><<<grid, 256, 0, st>>>(Mp, x, g_res, g_code, pwo, gam, bet, y, out); break;
+    case 4: k_cont_ln_v<TA, 4><<<grid, 256, 0, st>>>(Mp, x, g_res, g_code, pwo, gam, bet, y, out); break;
+    case 6: k_cont_ln_v<TA, 6><<<grid, 256, 0, st>>>(Mp, x, g_res, g_code, pwo, gam, bet, y, out); break;
+    case 8: k_cont_ln_v<TA, 8><<<grid, 256, 0, st>>>(Mp, x, g_res, g_code, pwo, gam, bet, y, out); break;
+    default:
+      k_cont_ln<TA><<<grid, 256, 0, st>>>(Mp, d, H, Q, x, g_res, g_code, pwo, gam, bet, y, out);
   }
 }
 

@@ -262,10 +262,10 @@ constexpr int TCA_SOFTMAX_WARPS = 4 * TCA_PARTS;
 constexpr int TCA_SOFTMAX_REGS = TCA_PARTS == 6 ? 72 : 96;
 constexpr int TCA_DRAIN_WARP0 = TCA_SOFTMAX_WARPS;
 constexpr int TCA_DRAIN_WARPS = TCA_PARTS == 6 ? 4 : 8;  // per row quadrant: 64 / 32 columns each
+constexpr int TCA_DRAIN_REGS = TCA_DRAIN_WARPS == 4 ? 48 : 40;
 constexpr int TCA_DRAIN_COLS = 64 * 4 / TCA_DRAIN_WARPS;
 constexpr int TCA_MMA_WARP = TCA_DRAIN_WARP0 + TCA_DRAIN_WARPS;
 constexpr int TCA_THREADS = 32 * (TCA_MMA_WARP + 4);
-constexpr int TCA_DRAIN_REGS = TCA_DRAIN_WARPS == 4 ? 48 : 40;
 
 __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
     const uint8_t* __restrict__ tinfo, const int32_t* __restrict__ n_tiles_p, int T, int d,
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
       uint32_t ph_free = 0, ph_p = 0;
       MTR_DECL
 #ifdef VQNQS_ATTN_TRACE2
-      uint32_t ph_sf = 1;  // S(0)'s phase is not waited for here
+      uint32_t ph_sf = 1, ph_pv = 0;  // S(0)'s phase is not waited for here
 #endif
       // S(0)
       tc::mbar_wait(&st_full[0], 0);
@@ -541,6 +541,11 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         MTR(5)
         issue_pv(it, hh, kb_cur, no_cur);
         MTR(6)
+#ifdef VQNQS_ATTN_TRACE2
+        tc::mbar_wait(pv_done, ph_pv);
+        ph_pv ^= 1;
+        MTR(0)
+#endif
         if (hh == hpg - 1) {  // item it's operands read
           if (leader) tc::mma_commit(&stage_free[it & 1]);
           __syncwarp();
@@ -933,6 +938,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           }
           tc::tmem_st8u(trow + TS_P + (sc_[i] >> 9), pk);
         }
+        ATR(4)
         tc::tmem_wait_st();
         ATR(6)
         tc::fence_before();
@@ -949,7 +955,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
              blockIdx.x, warp, nit, atr[0], atr[1], atr[2], atr[3], atr[4], atr[5], atr[6], atr[7],
              atr[11], atr[12], atr[8], atr[9]);
 #endif
-  }
+    }
   tc::fence_before();
   __syncthreads();
 #ifdef VQNQS_ATTN_TL
