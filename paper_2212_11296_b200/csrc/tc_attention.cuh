@@ -181,7 +181,7 @@ struct AttnSmem {
 // timeline mode: raw clock() of every trace point for three consecutive heads
 #define VQNQS_TL_H0 (200 + 24 * (int)blockIdx.x)
 #define ATR_DECL int tl_h = -1;
-#define ATR(k) { if ((unsigned)tl_h < 3u) tlog[warp][tl_h * 12 + (k)] = (unsigned)clock(); }
+#define ATR(k) { if ((unsigned)tl_h < 3u) tlog[warp][tl_h * 16 + (k)] = (unsigned)clock(); }
 #define MTR_DECL int tl_h = -VQNQS_TL_H0 - 1;
 #define MTR(k) ATR(k)
 #elif defined(VQNQS_ATTN_TRACE)
@@ -294,8 +294,8 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   __shared__ float2 red[2][TCA_PARTS][128];  // (local max, local sum)
   __shared__ float2 dnrm[128];       // drain warps' partial row norms
 #ifdef VQNQS_ATTN_TL
-  __shared__ unsigned tlog[32][36];
-  for (int i = threadIdx.x; i < 32 * 36; i += blockDim.x) (&tlog[0][0])[i] = 0;
+  __shared__ unsigned tlog[32][48];
+  for (int i = threadIdx.x; i < 32 * 48; i += blockDim.x) (&tlog[0][0])[i] = 0;
 #endif
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row = tid & 127, part = tid >> 7;  // warp w owns TMEM lanes 32(w%4)..
@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         float cm[TCA_SLOTS], cs[TCA_SLOTS];
         const int nl = __popc(sflags & 15u);
 #ifdef VQNQS_ATTN_TL
-        if ((unsigned)tl_h < 3u) tlog[warp][tl_h * 12 + 11] = 1000u + nl * 100 + (sflags >> 4);
+        if ((unsigned)tl_h < 3u) tlog[warp][tl_h * 16 + 11] = 1000u + nl * 100 + (sflags >> 4);
 #endif
 #if VQNQS_ATTN_SWP
         // Software pipeline inside the warp: chunk i + 1 is masked and reduced
@@ -909,6 +909,10 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
         float2 rq[TCA_PARTS];
 #pragma unroll
         for (int q = 0; q < TCA_PARTS; ++q) rq[q] = red[xb][q][row];
+#ifdef VQNQS_ATTN_TL
+        if (rq[0].x == 12345.f) ATR(13)  // keeps the loads before the stamp
+        ATR(12)
+#endif
         float m = rq[0].x;
 #pragma unroll
         for (int q = 1; q < TCA_PARTS; ++q) m = fmaxf(m, rq[q].x);
@@ -916,6 +920,10 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
 #pragma unroll
         for (int q = 0; q < TCA_PARTS; ++q)
           tot += rq[q].y > 0.f ? rq[q].y * ex2_approx((rq[q].x - m) * sl2) : 0.f;
+#ifdef VQNQS_ATTN_TL
+        if (tot == 12345.f) ATR(14)
+        ATR(13)
+#endif
         const float f = sp > 0.f ? __fdividef(ex2_approx((mp - m) * sl2), tot) : 0.f;
         ATR(4)
         // P is rewritten only after the previous head's value MMA consumed it
@@ -938,7 +946,7 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
           }
           tc::tmem_st8u(trow + TS_P + (sc_[i] >> 9), pk);
         }
-        ATR(4)
+        ATR(8)
         tc::tmem_wait_st();
         ATR(6)
         tc::fence_before();
@@ -962,14 +970,15 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   if (blockIdx.x < 8 && tid == 0 && nit * hpg > VQNQS_TL_H0 + 3) {
     unsigned t0 = 0xffffffffu;
     for (int w = 0; w < 32; ++w)
-      for (int e = 0; e < 36; ++e)
-        if (tlog[w][e] && tlog[w][e] < t0) t0 = tlog[w][e];
+      for (int e = 0; e < 48; ++e)
+        if ((e & 15) != 11 && tlog[w][e] && tlog[w][e] < t0) t0 = tlog[w][e];
     for (int w = 0; w < 32; ++w)
       for (int h = 0; h < 3; ++h) {
-        unsigned e[12];
-        for (int k = 0; k < 12; ++k) e[k] = tlog[w][h * 12 + k] ? tlog[w][h * 12 + k] - (k == 11 ? 0 : t0) : 0u;
-        printf("TL %d %d %d %u %u %u %u %u %u %u %u %u %u %u %u\n", (int)blockIdx.x, w, h, e[0], e[1],
-               e[2], e[3], e[4], e[5], e[6], e[7], e[8], e[9], e[10], e[11]);
+        unsigned e[16];
+        for (int k = 0; k < 16; ++k) e[k] = tlog[w][h * 16 + k] ? tlog[w][h * 16 + k] - (k == 11 ? 0 : t0) : 0u;
+        printf("TL %d %d %d %u %u %u %u %u %u %u %u %u %u %u %u %u %u %u %u\n", (int)blockIdx.x, w, h,
+               e[0], e[1], e[2], e[3], e[4], e[5], e[6], e[7], e[8], e[9], e[10], e[11], e[12],
+               e[13], e[14], e[15]);
       }
   }
 #endif
