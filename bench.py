@@ -391,7 +391,7 @@ def main():
         return {"bound": "tensor", "achieved": a, "peak": tpk, "unit": "TFLOP/s",
                 "frac": a / tpk, "other_bound": {"hbm_GBs": nbytes / secs / 1e9 if secs > 0
                                                  else 0.0, "frac": t_hbm / secs if secs else None}}
-    ncu_ref = load_ncu_traffic()
+    ncu_ref = load_ncu_traffic(w.name)
     tot_s, q_s = led.savings()
     f_alg = falg(w, led, prof_one)
     out = {
@@ -512,13 +512,18 @@ def mufu_roof(exps, secs, peaks) -> dict:
             "exps_per_step": exps}
 
 
-def load_ncu_traffic() -> dict:
+def load_ncu_traffic(workload: str) -> dict:
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-    kernels, from the committed `ncu --set full` capture summary."""
+    kernels, from the committed `ncu --set full` capture summary of THIS workload
+    (none committed for it: traffic is null)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
+        d = d.get("workloads", {}).get(workload) if "workloads" in d else \
+            (d if workload in d.get("source", "") else None)
+        if not d:
+            return {}
         return {k: v["dram_bytes_per_launch"] for k, v in d["kernels"].items()} | \
             {"source": d.get("source")}
     except Exception:

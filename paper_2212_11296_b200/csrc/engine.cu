@@ -481,6 +481,38 @@ class EngineImpl {
     size_chunks();
   }
 
+  // CUDA-core gathered attention (fp32 engine; bf16 engine when the tcgen05
+  // kernel does not take the shape): the register-blocked kernel for the head
+  // widths of the configurations, the one-query kernel otherwise.
+#ifndef VQNQS_ATTQ_NQ32
+#define VQNQS_ATTQ_NQ32 2
+#endif
+  template <typename TA, int DH, int NQ>
+  void launch_attention_q(int64_t R, int R1, int T, int d, int nh, float scale, const int32_t* Icur,
+                          const int64_t* Uo_cur, const TA* qkv, cudaStream_t st) {
+    const size_t asmem =
+        (((size_t(T) * (DH + 1) + 3) & ~size_t(3)) + size_t(T) * DH + 4 * size_t(T) * NQ + 4 * NQ * DH) * 4;
+    smem_optin(reinterpret_cast<const void*>(k_attention_q<TA, DH, NQ>), asmem);
+    k_attention_q<TA, DH, NQ><<<dim3(unsigned(R), nh), 128, asmem, st>>>(
+        R1, T, d, scale, K_.p, row_t1_.p, row_aoff_.p, act_off_.p, Icur, Uo_cur, qkv, att_.p);
+  }
+  template <typename TA>
+  void launch_attention_simt(int64_t R, int R1, int T, int d, int dh, int nh, float scale,
+                             const int32_t* Icur, const int64_t* Uo_cur, const TA* qkv,
+                             cudaStream_t st) {
+    switch (dh) {
+      case 8: launch_attention_q<TA, 8, 4>(R, R1, T, d, nh, scale, Icur, Uo_cur, qkv, st); return;
+      case 16: launch_attention_q<TA, 16, 4>(R, R1, T, d, nh, scale, Icur, Uo_cur, qkv, st); return;
+      case 32: launch_attention_q<TA, 32, VQNQS_ATTQ_NQ32>(R, R1, T, d, nh, scale, Icur, Uo_cur, qkv, st); return;
+      case 64: launch_attention_q<TA, 64, 2>(R, R1, T, d, nh, scale, Icur, Uo_cur, qkv, st); return;
+      default: break;
+    }
+    const size_t asmem = (size_t(T) * (dh + 1) + size_t(T) * dh + 4 * T + 4 * dh) * 4;
+    smem_optin(reinterpret_cast<const void*>(k_attention<TA>), asmem);
+    k_attention<TA><<<dim3(unsigned(R), nh), 128, asmem, st>>>(
+        R1, T, d, dh, scale, K_.p, row_t1_.p, row_aoff_.p, act_off_.p, Icur, Uo_cur, qkv, att_.p);
+  }
+
   template <typename TA>
   void gemm(const int64_t* Mp, int64_t Mcap, int Nn, int Kk, const void* A, int lda,
             const int32_t* gA, const void* B, const void* BT, const float* bias, void* out, int ldo,
@@ -639,11 +671,7 @@ class EngineImpl {
             tinfo_.p, ntiles_.p, T, d, dh, scale, reinterpret_cast<const bf16*>(qkv), att_hi_.p,
             att_lo_.p, xn2_.p, rr2_.p);
       } else {
-        const size_t asmem = (size_t(T) * (dh + 1) + size_t(T) * dh + 4 * T + 4 * dh) * 4;
-        smem_optin(reinterpret_cast<const void*>(k_attention<TA>), asmem);
-        k_attention<TA><<<dim3(unsigned(R), nh), 128, asmem, st>>>(
-            R1, T, d, dh, scale, K_.p, row_t1_.p, row_aoff_.p, act_off_.p, Icur, Uo_cur, qkv,
-            att_.p);
+        launch_attention_simt<TA>(R, R1, T, d, dh, nh, scale, Icur, Uo_cur, qkv, st);
       }
       CK(cudaEventRecord(lev[3 * b + 2], st));
       const int64_t* Mn = tot + 3 + b;

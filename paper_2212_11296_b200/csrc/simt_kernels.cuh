@@ -170,6 +170,167 @@ __global__ void __launch_bounds__(128) k_attention(
   }
 }
 
+#ifndef VQNQS_ATTQ_UNROLL
+#define VQNQS_ATTQ_UNROLL 4
+#endif
+constexpr int ATTQ_UNROLL = VQNQS_ATTQ_UNROLL;  // K/V fill loads in flight per thread
+// four consecutive operand elements as fp32 (16-byte / 8-byte aligned source)
+__device__ __forceinline__ float4 load4f(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ float4 load4f(const bf16* p) {
+  const uint2 w = *reinterpret_cast<const uint2*>(p);
+  return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u),
+                     __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xffff0000u));
+}
+
+// The same attention with NQ consecutive queries of the row per warp pass
+// (register-blocked: q of the NQ queries in registers, every K element read
+// from shared memory once per NQ products, every V element once per NQ
+// products, the NQ probabilities of a key as one vector load). Each score,
+// exponential, sum and output is formed by the same operations in the same
+// order as in k_attention, so the two kernels agree bit for bit.
+template <typename TA, int DH, int NQ>
+__global__ void __launch_bounds__(128) k_attention_q(
+    int R1, int T, int d, float scale, const int32_t* __restrict__ Ks,
+    const int32_t* __restrict__ row_t1, const int64_t* __restrict__ row_aoff,
+    const int64_t* __restrict__ act_off, const int32_t* __restrict__ I,
+    const int64_t* __restrict__ Uoff, const TA* __restrict__ qkv, float* __restrict__ att) {
+  extern __shared__ float sm[];
+  constexpr int NE = (DH + 31) / 32;  // output elements per lane
+  const int r = blockIdx.x, h = blockIdx.y;
+  const int s = r / R1, k = r % R1;
+  if (k >= Ks[s]) return;
+  const int a = k == 0 ? 0 : row_t1[r] + 1;
+  if (a >= T) return;
+  float* Kt = sm;                  // [T][DH+1]
+  float* Vt = Kt + ((T * (DH + 1) + 3) & ~3);  // [T][DH], 16-byte aligned
+  float* P = Vt + T * DH;          // [4][T][NQ]
+  float* Qs = P + 4 * T * NQ;      // [4][NQ][DH]
+  const int64_t base = act_off[s], rloc = base + row_aoff[r], uo = Uoff[s];
+  const int ld = 3 * d;
+  // K and V of the row's T positions, four elements per load
+#pragma unroll ATTQ_UNROLL
+  for (int idx = threadIdx.x; idx < T * (DH / 4); idx += blockDim.x) {
+    const int t = idx / (DH / 4), e = 4 * (idx % (DH / 4));
+    const int64_t loc = t < a ? base + t : rloc + (t - a);
+    const TA* src = qkv + (uo + I[loc]) * ld + d + h * DH + e;
+    const float4 kq = load4f(src), vq = load4f(src + d);
+    float* kr = Kt + t * (DH + 1) + e;
+    kr[0] = kq.x;
+    kr[1] = kq.y;
+    kr[2] = kq.z;
+    kr[3] = kq.w;
+    *reinterpret_cast<float4*>(Vt + t * DH + e) = vq;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* Pw = P + warp * T * NQ;
+  float* Qw = Qs + warp * NQ * DH;
+  for (int p0 = a + NQ * warp; p0 < T; p0 += 4 * NQ) {
+    const int nq = min(NQ, T - p0);   // live queries p0 .. p0 + nq - 1
+    const int pmax = p0 + nq - 1;
+    // q of the NQ queries: staged through shared memory, then in registers
+    for (int idx = lane; idx < NQ * DH; idx += 32) {
+      const int j = idx / DH, e = idx % DH;
+      float qv = 0.f;
+      if (j < nq) {
+        const int64_t u = uo + I[rloc + (p0 + j - a)];
+        qv = to_f<TA>(qkv[u * ld + h * DH + e]);
+      }
+      Qw[idx] = qv;
+    }
+    __syncwarp();
+    float q[NQ][DH];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j)
+#pragma unroll
+      for (int e = 0; e < DH; ++e) q[j][e] = Qw[j * DH + e];
+    float mx[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) mx[j] = -INFINITY;
+    for (int t = lane; t <= pmax; t += 32) {
+      float sc[NQ];
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) sc[j] = 0.f;
+      const float* kr = Kt + t * (DH + 1);
+#pragma unroll
+      for (int e = 0; e < DH; ++e) {
+        const float kv = kr[e];
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) sc[j] = fmaf(q[j][e], kv, sc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        sc[j] *= scale;
+        Pw[t * NQ + j] = sc[j];
+        if (t <= p0 + j) mx[j] = fmaxf(mx[j], sc[j]);
+      }
+    }
+    float sum[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      mx[j] = warp_max(mx[j]);
+      sum[j] = 0.f;
+    }
+    __syncwarp();
+    for (int t = lane; t <= pmax; t += 32) {
+#pragma unroll
+      for (int j = 0; j < NQ; ++j)
+        if (t <= p0 + j && j < nq) {
+          const float ev = expf(Pw[t * NQ + j] - mx[j]);
+          Pw[t * NQ + j] = ev;
+          sum[j] += ev;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) sum[j] = warp_sum(sum[j]);
+    for (int t = lane; t <= pmax; t += 32) {
+#pragma unroll
+      for (int j = 0; j < NQ; ++j)
+        if (t <= p0 + j && j < nq) Pw[t * NQ + j] = operand_round<TA>(Pw[t * NQ + j] / sum[j]);
+    }
+    __syncwarp();
+    // O = P V: lane e (and e + 32) of every live query; keys 0 .. p0 are
+    // common to the NQ queries, the last NQ - 1 keys are causal per query
+    float o[NQ][NE];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j)
+#pragma unroll
+      for (int c = 0; c < NE; ++c) o[j][c] = 0.f;
+    if (lane < DH) {
+      for (int t = 0; t <= p0; ++t) {
+        float pv[NQ];
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) pv[j] = Pw[t * NQ + j];
+#pragma unroll
+        for (int c = 0; c < NE; ++c) {
+          const float vv = Vt[t * DH + lane + 32 * c];
+#pragma unroll
+          for (int j = 0; j < NQ; ++j) o[j][c] = fmaf(pv[j], vv, o[j][c]);
+        }
+      }
+      for (int t = p0 + 1; t <= pmax; ++t) {
+#pragma unroll
+        for (int c = 0; c < NE; ++c) {
+          const float vv = Vt[t * DH + lane + 32 * c];
+#pragma unroll
+          for (int j = 1; j < NQ; ++j)
+            if (t <= p0 + j) o[j][c] = fmaf(Pw[t * NQ + j], vv, o[j][c]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NQ; ++j)
+        if (j < nq) {
+          const int64_t loc = rloc + (p0 + j - a);
+#pragma unroll
+          for (int c = 0; c < NE; ++c) att[loc * d + h * DH + lane + 32 * c] = o[j][c];
+        }
+    }
+    __syncwarp();
+  }
+}
+
 // Nearest codeword per location and VQ head (vq_apply_rows,
 // proj/src/model.cpp:283-319): argmin_j sum_c (x_c - W_jc)^2 in fp32 over one
 // head's d columns (row stride ldx), ties to the lowest j; the pick goes to

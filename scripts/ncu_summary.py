@@ -2,7 +2,7 @@
 
     python scripts/ncu_summary.py full  REP.ncu-rep[#i] OUT.txt # --set full capture (i-th kernel)
     python scripts/ncu_summary.py launches LAUNCHES.csv OUT.txt # gpu__time_duration list
-    python scripts/ncu_summary.py traffic OUT.json NAME=REP.ncu-rep ... --note "..."
+    python scripts/ncu_summary.py traffic OUT.json NAME=REP.ncu-rep[#i] ... --note "..." [--workload W]
 """
 import collections
 import csv
@@ -79,7 +79,9 @@ def launches(path, out):
     print("\n".join(lines))
 
 
-def traffic(out, pairs, note):
+def traffic(out, pairs, note, workload=None):
+    """Writes OUT as {"workloads": {WORKLOAD: {"source", "kernels"}}}, merging
+    into an existing file (bench.py reads the entry of the workload it runs)."""
     d = {"source": note, "kernels": {}}
     for p in pairs:
         name, rep = p.split("=", 1)
@@ -90,6 +92,15 @@ def traffic(out, pairs, note):
         tu = u[h.index("gpu__time_duration.sum")]
         d["kernels"][name] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                               "duration": f"{t} {tu}", "report": rep.split("/")[-1]}
+    if workload:
+        try:
+            allw = json.load(open(out))
+            if "workloads" not in allw:
+                allw = {"workloads": {}}
+        except Exception:
+            allw = {"workloads": {}}
+        allw["workloads"][workload] = d
+        d = allw
     json.dump(d, open(out, "w"), indent=1)
     print(json.dumps(d, indent=1))
 
@@ -107,4 +118,9 @@ if __name__ == "__main__":
             i = args.index("--note")
             note = args[i + 1]
             args = args[:i] + args[i + 2:]
-        traffic(sys.argv[2], args, note)
+        wl = None
+        if "--workload" in args:
+            i = args.index("--workload")
+            wl = args[i + 1]
+            args = args[:i] + args[i + 2:]
+        traffic(sys.argv[2], args, note, wl)
