@@ -55,6 +55,31 @@ inline void launch_tc_gemm_ws_bn(const int64_t* Mp, int64_t Mcap, int N, int K, 
                                      sms);
 }
 
+// W-stationary launcher (tc_gemm.cuh): bf16 epilogues, N % 256 == 0, the
+// resident W^T slice within the shared-memory budget.
+inline bool tc_gemm_wst_ok(int N, int K, int epi) {
+#ifdef VQNQS_NO_WST
+  return false;
+#endif
+  return (epi == EPI_STORE || epi == EPI_GELU) && N % TCS_BN == 0 && K % 64 == 0 &&
+         tcs_smem_bytes(K) <= smem_optin_limit();
+}
+template <int EPI>
+inline void launch_tc_gemm_wst(const int64_t* Mp, int64_t Mcap, int N, int K, const bf16* A,
+                               int lda, const bf16* WT, const float* bias, void* out, int ldo,
+                               cudaStream_t st, int sms) {
+  const size_t smem = tcs_smem_bytes(K);
+  smem_optin(reinterpret_cast<const void*>(k_tc_gemm_wst<EPI>), smem);
+  const CUtensorMap tmA = make_tmap_bf16(A, uint64_t(Mcap), uint64_t(K), 128, uint64_t(lda));
+  const CUtensorMap tmW = make_tmap_bf16(WT, uint64_t(N), uint64_t(K), TCS_BN);
+  const int tilesN = N / TCS_BN;
+  const int64_t tilesM = (Mcap + 127) / 128;
+  // a multiple of the slice count, at most one CTA per SM and per (slice, row tile)
+  const int per = int(std::max<int64_t>(1, std::min<int64_t>(tilesM, sms / tilesN)));
+  k_tc_gemm_wst<EPI><<<per * tilesN, TCW_THREADS, smem, st>>>(tmA, tmW, Mp, N, K, bias,
+                                                              static_cast<bf16*>(out), ldo);
+}
+
 inline void tc_gemm(const int64_t* Mp, int64_t Mcap, int N, int K, const void* A, int lda,
                     const int32_t* gA, const void* WT, const float* bias, void* out, int ldo,
                     int epi, const float* resid, int ldr, const int64_t* gR, cudaStream_t st,
@@ -62,6 +87,13 @@ inline void tc_gemm(const int64_t* Mp, int64_t Mcap, int N, int K, const void* A
   const bf16* a = static_cast<const bf16*>(A);
   const bf16* w = static_cast<const bf16*>(WT);
   if (gA || gR) throw std::runtime_error("tc_gemm: gathered operands are not supported");
+  if (tc_gemm_wst_ok(N, K, epi)) {
+    if (epi == EPI_GELU)
+      launch_tc_gemm_wst<EPI_GELU>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, st, sms);
+    else
+      launch_tc_gemm_wst<EPI_STORE>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, st, sms);
+    return;
+  }
   // warp-specialised TMA path (contiguous A rows, identity residual rows)
   if (N % 256 == 0)
     launch_tc_gemm_ws_bn<256>(Mp, Mcap, N, K, a, lda, w, bias, out, ldo, epi, resid, ldr, st, sms);
