@@ -27,8 +27,11 @@ def p(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
+# (20000, 1024, 256): several row tiles per CTA of the W-stationary kernel (K <= 256, N % 256 == 0);
+# N = 384 and K >= 768 take the streaming kernel
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 384, 128), (1000, 768, 256),
-                                   (77, 1024, 256), (513, 256, 1024), (4096, 2304, 768)])
+                                   (77, 1024, 256), (513, 256, 1024), (4096, 2304, 768),
+                                   (20000, 1024, 256)])
 @pytest.mark.parametrize("epi", [0, 1, 2])
 def test_tc_gemm_matches_torch(M, N, K, epi):
     L = _lib()
