@@ -145,12 +145,10 @@ extern "C" int vqnqs_debug_tc_attention(int S, int R1, int T, int d, int nh, con
   k_tile_info<<<sms * 8, 128>>>(tiles, ntiles, R1, T, row_t1, act_off, lrow, lpos, I, Uoff,
                                 tinfo);
   const size_t asmem = AttnSmem(T).total + 1024;
-  smem_optin(reinterpret_cast<const void*>(k_tc_attention), asmem);
-  k_tc_attention<<<sms, TCA_THREADS, asmem>>>(tinfo, ntiles, T, d, dh,
-                                              float(1.0 / std::sqrt(double(dh))),
-                                              static_cast<const bf16*>(qkv),
-                                              static_cast<bf16*>(xh), static_cast<bf16*>(xl),
-                                              xn2, rr2);
+  launch_tc_attention(dh, sms, asmem, (cudaStream_t)0, (const uint8_t*)tinfo,
+                      (const int32_t*)ntiles, T, d, dh, float(1.0 / std::sqrt(double(dh))),
+                      static_cast<const bf16*>(qkv), static_cast<bf16*>(xh),
+                      static_cast<bf16*>(xl), xn2, rr2);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) fprintf(stderr, "vqnqs_debug_tc_attention: %s\n", cudaGetErrorString(e));

@@ -666,10 +666,10 @@ class EngineImpl {
                                              lrow_.p, lpos_.p, Icur, Uo_cur, tinfo_.p);
         ++launches;
         const size_t asmem = AttnSmem(T).total + 1024;
-        smem_optin(reinterpret_cast<const void*>(k_tc_attention), asmem);
-        k_tc_attention<<<sms, TCA_THREADS, asmem, st>>>(
-            tinfo_.p, ntiles_.p, T, d, dh, scale, reinterpret_cast<const bf16*>(qkv), att_hi_.p,
-            att_lo_.p, xn2_.p, rr2_.p);
+        launch_tc_attention(dh, sms, asmem, st, (const uint8_t*)tinfo_.p,
+                            (const int32_t*)ntiles_.p, T, d, dh, scale,
+                            reinterpret_cast<const bf16*>(qkv), att_hi_.p, att_lo_.p, xn2_.p,
+                            rr2_.p);
       } else {
         launch_attention_simt<TA>(R, R1, T, d, dh, nh, scale, Icur, Uo_cur, qkv, st);
       }

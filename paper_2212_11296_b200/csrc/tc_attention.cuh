@@ -34,7 +34,7 @@
 // split xh = bf16(x), xl = bf16(x - xh) (the VQ distance GEMM operands; x is
 // represented to 2^-18 relative), |x|^2 and |x - xh - xl|^2 (the certified
 // argmin error bound, tc_vq.cuh). Warp w reads TMEM lanes 32(w%4).. (its
-// query rows); the warp roles are listed at TCA_THREADS.
+// query rows); the warp roles are listed above k_tc_attention.
 #pragma once
 
 #include "common.cuh"
@@ -261,16 +261,23 @@ static_assert(TCA_PARTS == 4 || TCA_PARTS == 6, "softmax warps per quadrant");
 constexpr int TCA_SOFTMAX_WARPS = 4 * TCA_PARTS;
 constexpr int TCA_SOFTMAX_REGS = TCA_PARTS == 6 ? 72 : 96;
 constexpr int TCA_DRAIN_WARP0 = TCA_SOFTMAX_WARPS;
-constexpr int TCA_DRAIN_WARPS = TCA_PARTS == 6 ? 4 : 8;  // per row quadrant: 64 / 32 columns each
-constexpr int TCA_DRAIN_REGS = TCA_DRAIN_WARPS == 4 ? 48 : 40;
-constexpr int TCA_DRAIN_COLS = 64 * 4 / TCA_DRAIN_WARPS;
-constexpr int TCA_MMA_WARP = TCA_DRAIN_WARP0 + TCA_DRAIN_WARPS;
-constexpr int TCA_THREADS = 32 * (TCA_MMA_WARP + 4);
+// Drain warps per CTA (template parameter NDRAIN): 4 (one per row quadrant,
+// 64 columns) when an item holds two or more heads (dh <= 32: an O buffer is
+// drained once per hpg heads, and four fewer warps compete with the softmax
+// warps: c4 +1.8%), 8 (two per quadrant, 32 columns each) when every head
+// ends an item (dh = 64: c5 is 4% slower with 4).
+constexpr int tca_threads(int ndrain) { return 32 * (TCA_DRAIN_WARP0 + ndrain + 4); }
+inline int tca_drain_warps(int dh) { return dh <= 32 ? 4 : 8; }
 
-__global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
+template <int NDRAIN>
+__global__ void __launch_bounds__(tca_threads(NDRAIN), 1) k_tc_attention(
     const uint8_t* __restrict__ tinfo, const int32_t* __restrict__ n_tiles_p, int T, int d,
     int dh, float scale, const bf16* __restrict__ qkv, bf16* __restrict__ xh_out,
     bf16* __restrict__ xl_out, float* __restrict__ xn2_out, float* __restrict__ rr2_out) {
+  constexpr int TCA_DRAIN_WARPS = NDRAIN;
+  constexpr int TCA_DRAIN_REGS = NDRAIN == 4 ? 48 : 40;
+  constexpr int TCA_DRAIN_COLS = 64 * 4 / NDRAIN;
+  constexpr int TCA_MMA_WARP = TCA_DRAIN_WARP0 + NDRAIN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -983,6 +990,18 @@ __global__ void __launch_bounds__(TCA_THREADS, 1) k_tc_attention(
   }
 #endif
   if (warp == 0) tc::tmem_dealloc(tmem, 512);
+}
+
+// launch with the drain-warp count of the head width
+template <class... Args>
+inline void launch_tc_attention(int dh, int grid, size_t smem, cudaStream_t st, Args... args) {
+  if (tca_drain_warps(dh) == 4) {
+    smem_optin(reinterpret_cast<const void*>(k_tc_attention<4>), smem);
+    k_tc_attention<4><<<grid, tca_threads(4), smem, st>>>(args...);
+  } else {
+    smem_optin(reinterpret_cast<const void*>(k_tc_attention<8>), smem);
+    k_tc_attention<8><<<grid, tca_threads(8), smem, st>>>(args...);
+  }
 }
 
 inline bool tc_attn_ok(int prec, int d, int dh, int T) {
